@@ -1,0 +1,385 @@
+"""Benchmark: voxel-iterations/s of the fused-lasso FISTA reconstruction
+(BASELINE.json metric) on the 1024x1024x512 high-concentration field (C3).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c3]
+
+One step = one complete fista() solve of the config (100 FISTA iterations on
+a synthetic hologram whose inputs are already resident in HBM).  N>1 runs are
+launched by torchrun; the volume is z-sharded over the ranks (weak scaling
+would fix planes/GPU; here the C3 volume is fixed, so scaling is "strong").
+The reference arm (--impl reference) times the CPU oracle port on the box's
+host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PITCH, DZ, Z0, LAM = 10e-6, 10e-6, 5e-3, 632e-9
+CONFIGS = {
+    # name: (nx, ny, nz, iters, shadow density, seed, lam_l1, lam_tv, inner, diameter)
+    "c1": (256, 256, 64, 50, None, 0, 0.5, 0.2, 5, 20e-6),
+    "c2": (1024, 1024, 256, 100, 0.05, 1, 0.5, 0.2, 5, 20e-6),
+    "c3": (1024, 1024, 512, 100, 0.2, 2, 0.5, 0.2, 5, 20e-6),
+    "c5": (1024, 1024, 512, 100, 0.05, 4, 0.05, 1.0, 20, 20e-6),
+}
+METRIC = "voxel-iterations/sec (1024²×512 fused-lasso FISTA) at 1/2/4/8 B200; % HBM roofline"
+BYTES_PER_VOXEL_ITER = 72  # SURVEY.md 8(d) algorithmic bytes per voxel-iteration
+# algorithmic HBM bytes per local voxel for one launch of each kernel class
+KERNEL_BYTES = {"prox": 32, "adj_cols": 8, "adj_rows": 16, "fwd_rows": 16, "fwd_cols": 8}
+
+
+def n_particles(cfg):
+    nx, _, _, _, sd, _, _, _, _, d = cfg
+    if sd is None:
+        return 50
+    return int(round(sd * (nx * PITCH) ** 2 / d ** 2))
+
+
+def render_gpu(points, nx, ny, diameter, device, batch=32):
+    """|1 - ifft2(sum_p fft2(disk_p) H(-z_p))|^2 (synth.py:161-181), float64 on the
+    GPU.  Benchmark-input generation only (not timed, not the hot path)."""
+    import torch
+    fy = torch.fft.fftfreq(ny, d=PITCH, dtype=torch.float64, device=device)[:, None]
+    fx = torch.fft.fftfreq(nx, d=PITCH, dtype=torch.float64, device=device)[None, :]
+    arg = 1.0 - (LAM * fx) ** 2 - (LAM * fy) ** 2
+    keep = arg >= 0
+    root = torch.sqrt(torch.clamp(arg, min=0.0))
+    xs = torch.arange(nx, dtype=torch.float64, device=device) * PITCH
+    ys = torch.arange(ny, dtype=torch.float64, device=device) * PITCH
+    spec = torch.zeros((ny, nx), dtype=torch.complex128, device=device)
+    pts = torch.as_tensor(points, dtype=torch.float64, device=device)
+    r2 = (diameter / 2.0) ** 2
+    for s in range(0, len(pts), batch):
+        p = pts[s:s + batch]
+        disk = ((xs[None, None, :] - p[:, 0, None, None]) ** 2 + (ys[None, :, None] - p[:, 1, None, None]) ** 2) <= r2
+        f = torch.fft.fft2(disk.to(torch.float64))
+        ph = (-2.0 * math.pi / LAM) * p[:, 2, None, None] * root[None]
+        spec += (f * torch.polar(keep.to(torch.float64).expand_as(ph), ph)).sum(0)
+    fld = torch.fft.ifft2(spec)
+    return (torch.abs(1.0 - fld) ** 2).cpu().numpy()
+
+
+def make_hologram(cfg, device):
+    from oracle.holo_oracle import Geometry, add_noise, invert_residual, make_scene
+    nx, ny, nz, _, _, seed, *_rest = cfg
+    d = cfg[9]
+    g = Geometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
+    pts = make_scene(n_particles(cfg), g, d, seed=seed, margin_planes=2)
+    img = render_gpu(pts, nx, ny, d, device)
+    return invert_residual(add_noise(img, 0.02, seed=seed + 7))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------- CPU arms ----
+
+def _cpu_sample(args):
+    b, nx, ny, nzs, iters, lam_l1, lam_tv, inner = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle.holo_oracle import Geometry, fista_solve
+    g = Geometry(nx, ny, nzs, PITCH, DZ, Z0, LAM)
+    t0 = time.perf_counter()
+    res = fista_solve(b, g, lam_l1=lam_l1, lam_tv=lam_tv, max_iters=iters, inner=inner,
+                      step_size=1.0 / (2.0 * nzs))
+    dt = time.perf_counter() - t0
+    return nx * ny * nzs * res.iterations, dt
+
+
+def cpu_sample_spec(cfg, planes=8, iters=1):
+    nx, ny, nz, _, _, _, l1, tv, inner, _ = cfg
+    return planes, iters, f"{nx}x{ny}x{planes} planes x {iters} FISTA iteration (step 1/(2*{planes})), " \
+                          f"same hologram, lambda=({l1},{tv}), T={inner}; per-voxel cost is nz-independent"
+
+
+def cpu_baseline(cfg, b):
+    planes, iters, desc = cpu_sample_spec(cfg)
+    nx, ny, _, _, _, _, l1, tv, inner, _ = cfg
+    vox, dt = _cpu_sample((b, nx, ny, planes, iters, l1, tv, inner))
+    return {"value": vox / dt, "unit": "voxel-iter/s", "cores": 1, "kind": "port",
+            "sample": desc + f"; {dt:.1f} s on 1 core"}
+
+
+def run_reference(a, cfg_name):
+    """--impl reference: the CPU oracle port (the reference is pure Python and
+    cannot travel to the box) on every host core, one independent solve per
+    core (like holotrack's `reconstruct --workers`)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cfg = CONFIGS[cfg_name]
+    nx, ny, nz, iters_full, _, seed, l1, tv, inner, d = cfg
+    from oracle.holo_oracle import Geometry, add_noise, invert_residual, make_scene
+    # bounded CPU render of a sample hologram: 400 particles keep it ~40 s
+    g = Geometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
+    rng_pts = make_scene(min(400, n_particles(cfg)), g, d, seed=seed, margin_planes=2)
+    from oracle.holo_oracle import render_hologram
+    b = invert_residual(add_noise(render_hologram(rng_pts, g, d), 0.02, seed=seed + 7))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    planes, iters, desc = cpu_sample_spec(cfg)
+    job = (b, nx, ny, planes, iters, l1, tv, inner)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(a.warmup):
+            pool.map(_cpu_sample, [job] * cores)
+        times = []
+        for _ in range(a.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_sample, [job] * cores)
+            times.append(time.perf_counter() - t0)
+    vox = sum(r[0] for r in res)
+    step_s = statistics.mean(times)
+    value = vox / step_s
+    line = {"metric": METRIC, "value": value, "unit": "voxel-iter/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg_name}: {nx}x{ny}x{nz}, {iters_full} iterations (sampled)",
+                       "sample": desc}, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
+                             "sample": desc + f"; {cores} concurrent solves (one per core)"},
+            "e2e": {"value": value, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm -----
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--iters", type=int, default=0, help="override FISTA iterations (0 = config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    a = ap.parse_args()
+    if a.impl == "reference":
+        run_reference(a, a.config)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1904_04884_b200 import _native as nat
+    from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, VolumeGeometry, fista
+    from paper_1904_04884_b200.engine import HoloEngine
+    from paper_1904_04884_b200.solver import native_config
+
+    cfg = CONFIGS[a.config]
+    nx, ny, nz, iters, _, seed, l1, tv, inner, d = cfg
+    if a.iters:
+        iters = a.iters
+    geom = VolumeGeometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
+    # identical synthetic hologram on every rank (seeded), generated on the GPU
+    b = make_hologram(cfg, dev) if rank == 0 or world == 1 else None
+    if world > 1:
+        bt = torch.as_tensor(b if b is not None else np.zeros((ny, nx)), dtype=torch.float64, device=dev)
+        dist.broadcast(bt, 0)
+        b = bt.cpu().numpy()
+    scfg = SolverConfig(weights=RegularizerWeights(l1, tv), max_iters=iters, tv_inner_iters=inner)
+    ncfg = native_config(scfg)
+    lib = nat.load()
+    if world > 1:
+        nid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            nat.check(lib.holo_nccl_unique_id(buf))
+            nid = torch.tensor(list(buf.raw), dtype=torch.uint8, device=dev)
+        dist.broadcast(nid, 0)
+        eng = HoloEngine(geom, local, shard=(rank, world, bytes(nid.cpu().tolist())))
+    else:
+        eng = HoloEngine(geom, local)
+    b_dev = torch.as_tensor(b, dtype=torch.float64, device=dev).contiguous()
+    stream = torch.cuda.current_stream(dev)
+
+    def one_solve():
+        code, rep, hist = eng.solve(b_dev, ncfg, stream=stream.cuda_stream)
+        return rep
+
+    for _ in range(a.warmup):
+        rep = one_solve()
+    lib.holo_profile_enable(eng.h, 1)
+    launches0 = lib.holo_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    vox_iters = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            rep = one_solve()
+            vox_iters += nx * ny * nz * rep.iterations
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = lib.holo_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # per-kernel-class device time recorded live during the timed region
+    n = ctypes.c_int32()
+    names = ctypes.create_string_buffer(32 * 16)
+    kms = (ctypes.c_double * 16)()
+    kcnt = (ctypes.c_int64 * 16)()
+    lib.holo_profile_read(eng.h, ctypes.byref(n), names, kms, kcnt)
+    lib.holo_profile_enable(eng.h, 0)
+    prof = {}
+    for i in range(n.value):
+        nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+        prof[nm] = {"ms": kms[i], "launches": int(kcnt[i])}
+
+    value = vox_iters / (ms / 1e3)
+    hbm, peak_kind = peaks()
+    local_vox = nx * ny * eng.nz_local
+    # dominant kernel by device time
+    dom = max((k for k in prof if k in KERNEL_BYTES), key=lambda k: prof[k]["ms"])
+    per_launch_s = prof[dom]["ms"] / 1e3 / max(prof[dom]["launches"], 1)
+    achieved = KERNEL_BYTES[dom] * local_vox / per_launch_s / 1e9
+    total_kernel_ms = sum(v["ms"] for v in prof.values())
+    step_roof = value / world * BYTES_PER_VOXEL_ITER / 1e9
+
+    # end to end through the public API with host buffers (pinned), N=1
+    e2e = None
+    if not a.no_e2e and world == 1:
+        pinned = torch.empty((ny, nx), dtype=torch.float64, pin_memory=True)
+        pinned.copy_(torch.as_tensor(b))
+        field = ComplexField2D.__new__(ComplexField2D)  # wrap the pinned buffer without a copy
+        field.values, field.pitch, field.wavelength = pinned.numpy(), PITCH, LAM
+        e2e_steps = max(1, min(a.steps, 2))
+        fista(field, geom, scfg)  # warm the public path
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e_vox, nnz = 0, 0
+        for _ in range(e2e_steps):
+            vol, rep_e = fista(field, geom, scfg)
+            e_vox += nx * ny * nz * rep_e.iterations
+            nnz = vol.nnz
+        e_s = time.perf_counter() - t0
+        e2e = {"value": e_vox / e_s, "unit": "voxel-iter/s", "h2d_bytes_per_step": 8 * nx * ny,
+               "d2h_bytes_per_step": 16 * nnz + 8 * nz + 8 * iters, "steps": e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, b)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "voxel-iter/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{a.config}: {nx}x{ny}x{nz} fused-lasso FISTA, {iters} iterations, "
+                                   f"{n_particles(cfg)} particles d=20um, lambda=({l1},{tv}), T={inner}",
+                       "l2": "inputs larger than L2 (state 3 x 4.3 GB complex64)", "parallelism": f"z-shard x{world}"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                         "alg_bytes_per_voxel": KERNEL_BYTES[dom]},
+            "step_roofline": {"bytes_per_voxel_iter": BYTES_PER_VOXEL_ITER, "achieved": step_roof, "peak": hbm,
+                              "frac": step_roof / hbm},
+            "kernels_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "kernel_share": {k: round(v["ms"] / total_kernel_ms, 4) for k, v in prof.items()} if total_kernel_ms else {},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "solve": {"iterations": rep.iterations, "restarts": rep.restarts, "nnz": rep.nnz,
+                      "final_sparsity": rep.final_sparsity, "attempts": rep.attempts},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

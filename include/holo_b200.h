@@ -1,0 +1,139 @@
+/* holo_b200.h -- C ABI of the B200 RIHVR fused-lasso FISTA hot path.
+ *
+ * Plain C: integers, doubles, opaque handles and raw pointers.  No torch or
+ * C++ types cross this boundary, and no C++ exception escapes it: every call
+ * returns a status code (HOLO_OK == 0) and holo_last_error() describes the
+ * most recent failure of the calling thread.
+ *
+ * The reference (holotrack, pure Python) has no native FFI of its own; these
+ * entry points replace the Python functions cited beside each one, so a
+ * ctypes/cffi binding slots in under the reference's public API
+ * (see INTEGRATION.md).  Citations are /root/reference/pkg/src/holotrack/...
+ *
+ * Conventions
+ *   - device pointers are CUDA device addresses on the handle's device;
+ *     complex data is interleaved float32 (re, im) = complex64, planes are
+ *     row-major (ny rows of nx samples), stacks plane-major.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the handle's stream).
+ *   - calls are stream-ordered; only calls returning host data synchronise.
+ *   - one handle per thread at a time.
+ */
+#ifndef HOLO_B200_H
+#define HOLO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOLO_OK 0
+#define HOLO_ERR_INVALID 1     /* bad argument: maps to ValueError                  */
+#define HOLO_ERR_UNSUPPORTED 2 /* shape/config this build does not handle: ValueError */
+#define HOLO_ERR_DIVERGED 3    /* objective > 1e6 f0: DivergenceError (report filled) */
+#define HOLO_ERR_CUDA 4        /* CUDA runtime error: RuntimeError                    */
+#define HOLO_ERR_NCCL 5        /* NCCL error: RuntimeError                            */
+
+#define HOLO_POLICY_BACKTRACKING 0
+#define HOLO_POLICY_FIXED 1
+
+typedef struct holo_handle holo_handle;
+
+/* optics.py:62-95 VolumeGeometry: plane k sits at z0 + k*dz. */
+typedef struct {
+  int32_t nx, ny, nz;
+  double pitch, dz, z0, wavelength;
+} holo_geometry;
+
+/* solver.py:38-68 SolverConfig (+ prox.py:26-35 RegularizerWeights).
+ * step_size <= 0 means "estimate" (solver.py:276-280). */
+typedef struct {
+  double lambda_l1, lambda_tv;
+  int32_t max_iters, tv_inner_iters;
+  int32_t step_policy;
+  double step_size;
+  double bt_shrink, stop_tol;
+  int32_t log_objective;
+} holo_solver_config;
+
+/* solver.py:71-85 SolveReport (+ counters the reference keeps internally). */
+typedef struct {
+  int32_t iterations, restarts, diverged, guard_fixups;
+  int32_t attempts; /* prox-gradient attempts incl. backtracking and restarts */
+  double step_size, final_sparsity, wall_time, f0;
+  int64_t nnz;
+} holo_report;
+
+const char* holo_last_error(void);
+int holo_version(void);
+/* 1 if this build handles the plane shape (FFT sizes: powers of two 8..4096) */
+int holo_shape_supported(int32_t nx, int32_t ny);
+
+/* Handle lifecycle.  holo_create: whole volume on one GPU.
+ * holo_create_sharded: planes [rank*nz/nranks, (rank+1)*nz/nranks) on this
+ * GPU, the forward plane-sum exchanged by an NCCL allreduce over the
+ * communicator built from `nccl_unique_id` (NCCL_UNIQUE_ID_BYTES = 128 bytes,
+ * made by holo_nccl_unique_id on rank 0 and broadcast by the caller). */
+int holo_create(const holo_geometry* geom, int device, holo_handle** out);
+int holo_nccl_unique_id(void* out128);
+int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_unique_id, int rank, int nranks,
+                        holo_handle** out);
+int holo_destroy(holo_handle* h);
+int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end);
+
+/* solver.py:225-247 estimate_operator_norm (complex engine): ||A||^2.  The
+ * complex engine has A A^H = nz * (band projector), so the power iteration
+ * converges to nz in one step; this returns that closed form.  The GPU
+ * power iteration itself is holo_power_iteration. */
+int holo_operator_norm(holo_handle* h, double* sigma2);
+int holo_power_iteration(holo_handle* h, int iters, uint64_t seed, double* sigma2);
+
+/* solver.py:254-379 fista (complex engine).  b: ny*nx real hologram residual
+ * (only Re(b) is used by the reference, solver.py:274).  _host reads a host
+ * buffer (copies inside); _device reads a device buffer of doubles. */
+int holo_solve(holo_handle* h, const double* b_host, const holo_solver_config* cfg, holo_report* rep);
+int holo_solve_device(holo_handle* h, const double* b_dev, const holo_solver_config* cfg, holo_report* rep,
+                      void* stream);
+/* objective history of the last solve (solver.py:353); n = entries */
+int holo_history(const holo_handle* h, double* out, int32_t cap, int32_t* n);
+
+/* sparsevol.py:75-88 from_dense over the solution: nnz per local plane, then
+ * COO entries sorted by (plane, row, col); vals are complex64 pairs.
+ * _host copies into host buffers, _device fills device buffers. */
+int holo_plane_nnz(holo_handle* h, int64_t* nnz_per_local_plane);
+int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz);
+int holo_export_coo_device(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz,
+                           void* stream);
+/* device pointer to the dense complex64 solution (local planes) */
+int holo_solution_device(holo_handle* h, void** x);
+
+/* ---- operator-level entry points (parity tests; device pointers) ---- */
+/* optics.py:146-169 TransferLadder.stack(k0, k1, conj) as complex64 */
+int holo_op_transfer(holo_handle* h, int32_t k0, int32_t k1, int32_t conj, void* out, void* stream);
+/* numpy fft2 / ifft2 (1/P scaled) of nplanes complex64 planes, in place */
+int holo_op_fft2(holo_handle* h, void* data, int32_t nplanes, int32_t inverse, void* stream);
+/* solver.py:110-124 forward_sparse: out (float32, ny*nx) = Re ifft2(sum_k fft2(x_k) conj(H_k));
+ * x = local planes (complex64).  Sharded handles allreduce the plane sum. */
+int holo_op_forward(holo_handle* h, const void* x, void* out, void* stream);
+/* optics.py:215-230 adjoint: out[k] = scale * ifft2(H_k fft2(r)), r float32 ny*nx,
+ * out = local planes complex64 (scale 2 reproduces solver.py:126-132) */
+int holo_op_adjoint(holo_handle* h, const void* r, void* out, double scale, void* stream);
+/* prox.py:151-165 prox_fl over nplanes complex64 planes of any (ny, nx):
+ * soft-threshold(tau_l1) of the FGP-TV prox (tau_tv, inner) of re and im,
+ * including the per-plane guard (prox.py:138-147). */
+int holo_op_prox_fl(holo_handle* h, const void* v, void* out, int32_t nplanes, int32_t ny, int32_t nx, double tau_l1,
+                    double tau_tv, int32_t inner, void* stream);
+
+/* ---- instrumentation ---- */
+/* per-kernel-class device time (CUDA events on the launching stream) */
+int holo_profile_enable(holo_handle* h, int32_t on);
+/* n = #classes; names: n x 32 bytes; ms: accumulated device ms; counts: launches */
+int holo_profile_read(holo_handle* h, int32_t* n, char* names, double* ms, int64_t* counts);
+/* kernels launched by this library since it was loaded (all handles) */
+int64_t holo_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOLO_B200_H */

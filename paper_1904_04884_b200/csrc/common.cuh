@@ -1,0 +1,73 @@
+// Shared device helpers: complex float2 arithmetic, the fixed-point transfer
+// phase, and deterministic fp64 block reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define HD __device__ __forceinline__
+
+namespace holo {
+
+HD float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+HD float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+HD float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+HD float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+HD float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+HD float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+HD float2 czero() { return make_float2(0.f, 0.f); }
+
+// exp(2*pi*i * ph / 2^64).  ph is the transfer phase in cycles as a 64-bit
+// binary fraction, so "mod 1" is free integer wrap-around.  The top 8 bits
+// index a 256-entry unit-circle table (fp64-exact entries); the remaining
+// < 2^-8 cycle is a short Taylor rotation (|theta| < 0.0246 rad, truncation
+// error < 1e-10).  Max error vs exact ~2 ulp of fp32.
+HD float2 cis_cycles(uint64_t ph, const float2* __restrict__ circle256) {
+  const uint32_t c = (uint32_t)(ph >> 32);
+  const float2 base = circle256[c >> 24];
+  const float th = (float)(c & 0xFFFFFFu) * 1.4629180792671596e-09f;  // 2*pi / 2^32
+  const float th2 = th * th;
+  const float cs = fmaf(th2, fmaf(th2, 1.0f / 24.0f, -0.5f), 1.0f);
+  const float sn = th * fmaf(th2, -1.0f / 6.0f, 1.0f);
+  return make_float2(fmaf(base.x, cs, -base.y * sn), fmaf(base.x, sn, base.y * cs));
+}
+
+// Phase of plane k at one pixel: A + k*B (mod 2^64); A, B = frac(z0*q), frac(dz*q).
+HD uint64_t plane_phase(ulonglong2 ab, int k) {
+  return ab.x + (uint64_t)(uint32_t)k * ab.y;
+}
+
+// Deterministic block reduction of NV doubles per thread; thread 0..NV-1 of
+// warp 0 end up holding the block sums in out[] (written to global by caller).
+template <int NV, int NT>
+HD void block_sum(double (&v)[NV], double* __restrict__ dst) {
+  static_assert(NT % 32 == 0, "block must be whole warps");
+  constexpr int NW = NT / 32;
+  __shared__ double red[NW][NV];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    v[i] = x;
+  }
+  __syncthreads();  // red[] may be reused by a previous call
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[w][i] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) s += red[k][threadIdx.x];
+    dst[threadIdx.x] = s;
+  }
+}
+
+}  // namespace holo

@@ -1,0 +1,876 @@
+// Device-resident FISTA engine and the extern "C" boundary (include/holo_b200.h).
+//
+// The outer loop restates solver.py:254-379 (complex engine) on the host in
+// C++; every O(volume) operation runs in the sm_100a kernels of kernels.cu.
+// Per outer iteration the host reads back one small block of fp64 scalars.
+//
+// State layout in HBM (per rank, nzl local planes, P = ny*nx):
+//   X[3]      nzl*P complex64  -- x_k, x_{k-1}, candidate (rotating slots)
+//   S[3]      P complex64      -- sensor spectra A x of the three slots
+//   scratch   nzl*P complex64  -- adjoint gradient / forward row-pass output
+//   Spart     G*P complex64    -- per-group forward partial spectra
+//   Bspec, R  P complex64      -- FFT(b) and the masked residual spectrum
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifdef HOLO_WITH_NCCL
+#include <nccl.h>
+#endif
+
+#include "../../include/holo_b200.h"
+#include "kernels.cuh"
+
+namespace holo {
+
+static thread_local std::string g_err;
+
+struct Status {
+  int code = HOLO_OK;
+  static Status ok() { return Status(); }
+};
+
+#define HOLO_CUDA(expr)                                                                    \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      g_err = std::string(#expr) + ": " + cudaGetErrorString(_e);                          \
+      return HOLO_ERR_CUDA;                                                                \
+    }                                                                                      \
+  } while (0)
+
+#ifdef HOLO_WITH_NCCL
+#define HOLO_NCCL(expr)                                                                    \
+  do {                                                                                     \
+    ncclResult_t _r = (expr);                                                              \
+    if (_r != ncclSuccess) {                                                               \
+      g_err = std::string(#expr) + ": " + ncclGetErrorString(_r);                          \
+      return HOLO_ERR_NCCL;                                                                \
+    }                                                                                      \
+  } while (0)
+#endif
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class T>
+static cudaError_t dalloc(T*& p, size_t count) {
+  if (p) return cudaSuccess;
+  return cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1));
+}
+
+// Per-kernel-class device timing with CUDA events on the launching stream
+// (enabled by holo_profile_enable; harvested at each host sync point).
+enum ProfKind { PK_ADJ_COLS = 0, PK_ADJ_ROWS, PK_PROX, PK_FWD_ROWS, PK_FWD_COLS, PK_SUM_GROUPS, PK_SENSOR, PK_REDUCE, PK_N };
+static const char* kProfNames[PK_N] = {"adj_cols", "adj_rows", "prox", "fwd_rows",
+                                       "fwd_cols", "sum_groups", "sensor", "reduce"};
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;
+  int used = 0;
+  double ms[PK_N] = {};
+  long long cnt[PK_N] = {};
+  void reset() {
+    for (int i = 0; i < PK_N; ++i) { ms[i] = 0; cnt[i] = 0; }
+  }
+  cudaError_t begin(int k, cudaStream_t s) {
+    if (!on) return cudaSuccess;
+    if ((int)kind.size() <= used) {
+      cudaEvent_t a, b;
+      cudaError_t e;
+      if ((e = cudaEventCreate(&a))) return e;
+      if ((e = cudaEventCreate(&b))) return e;
+      ev.push_back(a);
+      ev.push_back(b);
+      kind.push_back(0);
+    }
+    kind[used] = k;
+    return cudaEventRecord(ev[2 * used], s);
+  }
+  cudaError_t end(cudaStream_t s) {
+    if (!on) return cudaSuccess;
+    cudaError_t e = cudaEventRecord(ev[2 * used + 1], s);
+    ++used;
+    return e;
+  }
+  // call after the stream has been synchronised
+  cudaError_t harvest() {
+    for (int i = 0; i < used; ++i) {
+      float t = 0.f;
+      cudaError_t e = cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
+      if (e) return e;
+      ms[kind[i]] += t;
+      cnt[kind[i]] += 1;
+    }
+    used = 0;
+    return cudaSuccess;
+  }
+  ~Prof() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+#define PROF(kindv, s, call)                 \
+  do {                                       \
+    HOLO_CUDA(prof.begin((kindv), (s)));     \
+    HOLO_CUDA(call);                         \
+    HOLO_CUDA(prof.end((s)));                \
+  } while (0)
+
+// host scalar block (pinned) layout
+enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_N };
+
+struct Engine {
+  holo_geometry geom{};
+  int device = 0, rank = 0, nranks = 1, kb = 0, ke = 0, nzl = 0;
+  long long P = 0;
+  cudaStream_t stream = nullptr;
+  Plan plan;
+#ifdef HOLO_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // volume buffers
+  float2* X[3] = {nullptr, nullptr, nullptr};
+  float2* scratch = nullptr;
+  float2* Spart = nullptr;
+  int groups = 1;
+  // plane-sized buffers
+  float2* S[3] = {nullptr, nullptr, nullptr};
+  float2* Bspec = nullptr;
+  float2* R = nullptr;
+  double* b64 = nullptr;
+  // reductions
+  double* sens_part = nullptr;
+  int sens_nblk = 0;
+  double* scal = nullptr;       // device scalars [SC_N]
+  double* h_scal = nullptr;     // pinned mirror
+  double* prox_part = nullptr;  // [nzl][tpp][kProxParts]
+  size_t prox_part_cap = 0;
+  double* plane_out = nullptr;  // [nzl][4]
+  int* new_fail = nullptr;      // [nzl]
+  uint8_t* force_acc = nullptr; // [nzl]
+  float* fgp_beta = nullptr;
+  int fgp_cap = 0;
+  // coo
+  int* coo_counts = nullptr;
+  long long* coo_offsets = nullptr;
+  std::vector<int> h_counts;
+  std::vector<long long> h_offsets;
+  // results of the last solve
+  int ix = 0;  // slot holding the solution
+  bool have_solution = false;
+  std::vector<double> history;
+  holo_report last{};
+  Prof prof;
+
+  ~Engine() { release(); }
+
+  void release() {
+    for (auto& p : X) cudaFree(p);
+    for (auto& p : S) cudaFree(p);
+    cudaFree(scratch); cudaFree(Spart); cudaFree(Bspec); cudaFree(R); cudaFree(b64);
+    cudaFree(sens_part); cudaFree(scal); cudaFreeHost(h_scal); cudaFree(prox_part);
+    cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(fgp_beta);
+    cudaFree(coo_counts); cudaFree(coo_offsets);
+    plan_free(plan);
+#ifdef HOLO_WITH_NCCL
+    if (comm) ncclCommDestroy(comm);
+    comm = nullptr;
+#endif
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+  }
+
+  cudaStream_t st(void* s) const { return s ? (cudaStream_t)s : stream; }
+
+  int init(const holo_geometry& g, int dev, int r, int n) {
+    geom = g;
+    device = dev;
+    rank = r;
+    nranks = n;
+    if (g.nx < 1 || g.ny < 1 || g.nz < 1) return fail(HOLO_ERR_INVALID, "voxel counts must be >= 1");
+    if (!(g.pitch > 0) || !(g.dz > 0) || !(g.wavelength > 0)) return fail(HOLO_ERR_INVALID, "pitch, dz and wavelength must be positive");
+    if (g.z0 < 0) return fail(HOLO_ERR_INVALID, "z0 must be nonnegative");
+    if (!plan_supported(g.nx, g.ny))
+      return fail(HOLO_ERR_UNSUPPORTED, "plane shape " + std::to_string(g.ny) + "x" + std::to_string(g.nx) +
+                                            " unsupported: the B200 FFT handles powers of two in [8, 4096]");
+    if (n < 1 || r < 0 || r >= n) return fail(HOLO_ERR_INVALID, "bad rank/nranks");
+    kb = (int)((long long)g.nz * r / n);
+    ke = (int)((long long)g.nz * (r + 1) / n);
+    nzl = ke - kb;
+    P = (long long)g.nx * g.ny;
+    HOLO_CUDA(cudaSetDevice(dev));
+    HOLO_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    HOLO_CUDA(plan_build(plan, g.nx, g.ny, g.nz, g.pitch, g.dz, g.z0, g.wavelength, stream));
+    HOLO_CUDA(cudaMalloc(&scal, sizeof(double) * SC_N));
+    HOLO_CUDA(cudaMallocHost(&h_scal, sizeof(double) * SC_N));
+    sens_nblk = sensor_blocks(plan);
+    HOLO_CUDA(cudaMalloc(&sens_part, sizeof(double) * std::max(sens_nblk, 2048)));
+    return HOLO_OK;
+  }
+
+  int ensure_planes() {
+    for (auto& p : S) HOLO_CUDA(dalloc(p, P));
+    HOLO_CUDA(dalloc(Bspec, P));
+    HOLO_CUDA(dalloc(R, P));
+    HOLO_CUDA(dalloc(b64, P));
+    return HOLO_OK;
+  }
+
+  int ensure_scratch() {
+    HOLO_CUDA(dalloc(scratch, (size_t)nzl * P));
+    groups = fwd_groups(plan, std::max(nzl, 1));
+    HOLO_CUDA(dalloc(Spart, (size_t)groups * P));
+    return ensure_planes();
+  }
+
+  int ensure_volume() {
+    for (auto& p : X) HOLO_CUDA(dalloc(p, (size_t)nzl * P));
+    HOLO_CUDA(dalloc(plane_out, (size_t)std::max(nzl, 1) * 4));
+    HOLO_CUDA(dalloc(new_fail, std::max(nzl, 1)));
+    HOLO_CUDA(dalloc(force_acc, std::max(nzl, 1)));
+    return ensure_scratch();
+  }
+
+  int ensure_prox(ProxArgs& a, int nplanes, int ny, int nx, int inner, cudaStream_t s) {
+    prox_setup(a, ny, nx, inner);
+    a.nplanes = nplanes;
+    if (!prox_supported(ny, nx, inner))
+      return fail(HOLO_ERR_UNSUPPORTED, "tv_inner_iters=" + std::to_string(inner) + " too deep for the single-pass prox tile");
+    const size_t need = (size_t)std::max(nplanes, 1) * a.tiles_per_plane * kProxParts;
+    if (need > prox_part_cap) {
+      cudaFree(prox_part);
+      prox_part = nullptr;
+      HOLO_CUDA(cudaMalloc(&prox_part, sizeof(double) * need));
+      prox_part_cap = need;
+    }
+    a.part = prox_part;
+    if (inner > fgp_cap) {
+      cudaFree(fgp_beta);
+      fgp_beta = nullptr;
+      HOLO_CUDA(cudaMalloc(&fgp_beta, sizeof(float) * inner));
+      fgp_cap = inner;
+    }
+    // data-independent FGP momentum (prox.py:132-133)
+    std::vector<float> bt(inner);
+    double t = 1.0;
+    for (int i = 0; i < inner; ++i) {
+      const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+      bt[i] = (float)((t - 1.0) / tn);
+      t = tn;
+    }
+    HOLO_CUDA(cudaMemcpyAsync(fgp_beta, bt.data(), sizeof(float) * inner, cudaMemcpyHostToDevice, s));
+    HOLO_CUDA(cudaStreamSynchronize(s));  // bt is a stack buffer
+    a.fgp_beta = fgp_beta;
+    return HOLO_OK;
+  }
+
+  // ---- collectives (no-ops on one rank) ----
+  int allreduce_spec(float2* spec, cudaStream_t s) {
+    if (nranks == 1) return HOLO_OK;
+#ifdef HOLO_WITH_NCCL
+    HOLO_NCCL(ncclAllReduce(spec, spec, (size_t)P * 2, ncclFloat, ncclSum, comm, s));
+    return HOLO_OK;
+#else
+    return fail(HOLO_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+  }
+  int allreduce_scalars(double* d, int n, cudaStream_t s) {
+    if (nranks == 1) return HOLO_OK;
+#ifdef HOLO_WITH_NCCL
+    HOLO_NCCL(ncclAllReduce(d, d, n, ncclDouble, ncclSum, comm, s));
+    return HOLO_OK;
+#else
+    return fail(HOLO_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+  }
+
+  // S_out = A x (spectrum, band mask not applied; allreduced over ranks)
+  int forward_spectrum(const float2* x, float2* S_out, cudaStream_t s) {
+    PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzl * geom.ny, false, 1.0f, s));
+    PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzl, kb, groups, s));
+    PROF(PK_SUM_GROUPS, s, sum_groups(plan, Spart, groups, S_out, s));
+    return allreduce_spec(S_out, s);
+  }
+
+  // scratch = 2 A^H r with R the masked residual spectrum
+  int adjoint_grad(const float2* Rm, float scale, cudaStream_t s) {
+    PROF(PK_ADJ_COLS, s, adj_cols(plan, Rm, scratch, nzl, kb, s));
+    PROF(PK_ADJ_ROWS, s, fft_rows(plan, scratch, scratch, (long long)nzl * geom.ny, true, scale / (float)P, s));
+    return HOLO_OK;
+  }
+
+  int load_b(const double* b_dev, cudaStream_t s) {
+    int rc = ensure_volume();
+    if (rc) return rc;
+    int nblk = 0;
+    HOLO_CUDA(load_hologram(b_dev, Bspec, P, sens_part, &nblk, s));
+    HOLO_CUDA(final_sum(sens_part, nblk, 1.0, scal + SC_F0, s));
+    // Bspec = fft2(b)
+    HOLO_CUDA(fft_rows(plan, Bspec, Bspec, geom.ny, false, 1.0f, s));
+    HOLO_CUDA(fft_cols(plan, Bspec, Bspec, 1, false, 1.0f, s));
+    return HOLO_OK;
+  }
+
+  int read_scalars(cudaStream_t s) {
+    HOLO_CUDA(cudaMemcpyAsync(h_scal, scal, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, s));
+    HOLO_CUDA(cudaStreamSynchronize(s));
+    HOLO_CUDA(prof.harvest());
+    return HOLO_OK;
+  }
+
+  struct Attempt {
+    int slot;
+    double f_new, f_y, step, pen, ip, dx2;
+  };
+
+  // prox + reductions for one attempt, writes candidate into X[c]
+  int prox_step(ProxArgs& a, cudaStream_t s) {
+    PROF(PK_PROX, s, prox(a, s));
+    HOLO_CUDA(prof.begin(PK_REDUCE, s));
+    HOLO_CUDA(prox_reduce(a, a.tau_tv, a.tau_tv > 0.f, force_acc, plane_out, new_fail, s));
+    HOLO_CUDA(plane_total(plane_out, new_fail, nzl, scal, s));
+    HOLO_CUDA(prof.end(s));
+    return allreduce_scalars(scal, SC_FAIL + 1, s);
+  }
+
+  // solver.py:297-327 iterate_from(y, step) with y = (1+beta) x - beta xp
+  int iterate_from(int sx, int sxp, double beta, double step, const holo_solver_config& cfg, Attempt& out,
+                   cudaStream_t s) {
+    int rc;
+    const bool mom = beta != 0.0;
+    // residual spectrum at y (linearity: S_y = (1+beta) S_x - beta S_xp)
+    HOLO_CUDA(prof.begin(PK_SENSOR, s));
+    HOLO_CUDA(sensor(plan, S[sx], mom ? S[sxp] : nullptr, (float)(1.0 + beta), (float)(-beta), Bspec, R, sens_part, s));
+    HOLO_CUDA(final_sum(sens_part, sens_nblk, 1.0 / (double)P, scal + SC_FY, s));
+    HOLO_CUDA(prof.end(s));
+    int c = 0;
+    while (c == sx || c == sxp) ++c;
+    const double sigma2 = (double)geom.nz;  // ||A||^2, closed form (see holo_operator_norm)
+    for (;;) {
+      // gradient 2 A^H r_y into scratch (the forward pass below reuses scratch,
+      // so a backtracking retry recomputes it)
+      if ((rc = adjoint_grad(R, 2.0f, s))) return rc;
+      ProxArgs a;
+      if ((rc = ensure_prox(a, nzl, geom.ny, geom.nx, cfg.tv_inner_iters, s))) return rc;
+      a.x = X[sx];
+      a.xp = X[sxp];
+      a.grad = scratch;
+      a.xnew = X[c];
+      a.beta = (float)beta;
+      a.step = (float)step;
+      a.tau_l1 = (float)(step * cfg.lambda_l1);
+      a.tau_tv = (float)(step * cfg.lambda_tv);
+      a.lr_tv = a.tau_tv > 0.f ? (float)(1.0 / (8.0 * (step * cfg.lambda_tv))) : 0.f;
+      HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzl, 1), s));
+      if ((rc = prox_step(a, s))) return rc;
+      if ((rc = read_scalars(s))) return rc;
+      // guard fix-up: planes whose TV output was worse than its input take the
+      // identity for that part (prox.py:138-147); rare, so handled out of line
+      while (h_scal[SC_FAIL] > 0.5) {
+        last.guard_fixups += 1;
+        ProxArgs f = a;
+        f.force = force_acc;
+        if ((rc = prox_step(f, s))) return rc;
+        if ((rc = read_scalars(s))) return rc;
+      }
+      last.attempts += 1;
+      // forward of the candidate; the adjoint scratch is consumed, reuse it
+      if ((rc = forward_spectrum(X[c], S[c], s))) return rc;
+      HOLO_CUDA(prof.begin(PK_SENSOR, s));
+      HOLO_CUDA(sensor(plan, S[c], nullptr, 1.f, 0.f, Bspec, nullptr, sens_part, s));
+      HOLO_CUDA(final_sum(sens_part, sens_nblk, 1.0 / (double)P, scal + SC_FNEW, s));
+      HOLO_CUDA(prof.end(s));
+      if ((rc = read_scalars(s))) return rc;
+      out.slot = c;
+      out.f_new = h_scal[SC_FNEW];
+      out.f_y = h_scal[SC_FY];
+      out.step = step;
+      out.ip = h_scal[SC_IP];
+      out.dx2 = h_scal[SC_DX2];
+      out.pen = cfg.lambda_l1 * h_scal[SC_L1] + (cfg.lambda_tv > 0 ? cfg.lambda_tv * h_scal[SC_TV] : 0.0);
+      if (cfg.step_policy != HOLO_POLICY_BACKTRACKING) return HOLO_OK;
+      // Sufficient-decrease test of solver.py:324-326.  With ||A||^2 = nz the
+      // exact slack f_new - bound = ||A d||^2 - ||d||^2/(2 step) is <= 0 for
+      // every step <= 1/(2 nz), so the reference (fp64, 1e-12 relative slack)
+      // accepts; evaluating it in fp32 would only add rounding noise.
+      if (2.0 * sigma2 * step <= 1.0 + 1e-14) return HOLO_OK;
+      const double bound = out.f_y + out.ip + out.dx2 / (2.0 * step);
+      if (out.f_new <= bound + 1e-12 * std::max(1.0, std::fabs(bound)) || step < 1e-30) return HOLO_OK;
+      step *= cfg.bt_shrink;
+    }
+  }
+
+  int count_nnz(int slot, long long& total, std::vector<long long>* per_plane, cudaStream_t s) {
+    const int nch = coo_chunks(P, std::max(nzl, 1));
+    HOLO_CUDA(dalloc(coo_counts, nch));
+    HOLO_CUDA(dalloc(coo_offsets, nch));
+    h_counts.resize(nch);
+    h_offsets.resize(nch);
+    if (nzl == 0) {
+      total = 0;
+      if (per_plane) per_plane->clear();
+      return HOLO_OK;
+    }
+    HOLO_CUDA(coo_count(X[slot], P, nzl, coo_counts, s));
+    HOLO_CUDA(cudaMemcpyAsync(h_counts.data(), coo_counts, sizeof(int) * nch, cudaMemcpyDeviceToHost, s));
+    HOLO_CUDA(cudaStreamSynchronize(s));
+    const int cpp = nch / nzl;
+    long long run = 0;
+    if (per_plane) per_plane->assign(nzl, 0);
+    for (int i = 0; i < nch; ++i) {
+      h_offsets[i] = run;
+      run += h_counts[i];
+      if (per_plane) (*per_plane)[i / cpp] += h_counts[i];
+    }
+    total = run;
+    HOLO_CUDA(cudaMemcpyAsync(coo_offsets, h_offsets.data(), sizeof(long long) * nch, cudaMemcpyHostToDevice, s));
+    return HOLO_OK;
+  }
+
+  // solver.py:254-379
+  int solve(const double* b_dev, const holo_solver_config& cfg, holo_report& rep, cudaStream_t s) {
+    auto t0 = std::chrono::steady_clock::now();
+    int rc;
+    if (cfg.max_iters < 1) return fail(HOLO_ERR_INVALID, "max_iters must be >= 1");
+    if (cfg.tv_inner_iters < 1) return fail(HOLO_ERR_INVALID, "tv_inner_iters must be >= 1");
+    if (!(cfg.bt_shrink > 0.0 && cfg.bt_shrink < 1.0)) return fail(HOLO_ERR_INVALID, "bt_shrink must be in (0, 1)");
+    if (cfg.lambda_l1 < 0 || cfg.lambda_tv < 0) return fail(HOLO_ERR_INVALID, "regularizer weights must be nonnegative");
+    if (cfg.stop_tol < 0) return fail(HOLO_ERR_INVALID, "stop_tol must be nonnegative");
+    if (cfg.step_policy != HOLO_POLICY_BACKTRACKING && cfg.step_policy != HOLO_POLICY_FIXED)
+      return fail(HOLO_ERR_INVALID, "unknown step_policy");
+    if ((rc = load_b(b_dev, s))) return rc;
+    last = holo_report{};
+    history.clear();
+    have_solution = false;
+    const size_t vbytes = sizeof(float2) * (size_t)nzl * P;
+    for (int i = 0; i < 3; ++i) {
+      if (vbytes) HOLO_CUDA(cudaMemsetAsync(X[i], 0, vbytes, s));
+      HOLO_CUDA(cudaMemsetAsync(S[i], 0, sizeof(float2) * P, s));
+    }
+    if ((rc = read_scalars(s))) return rc;
+    const double f0 = h_scal[SC_F0];
+    double step;
+    if (cfg.step_size > 0) {
+      step = cfg.step_size;
+    } else {
+      const double sigma2 = (double)geom.nz;
+      step = sigma2 > 0 ? 1.0 / (2.0 * sigma2) : 1.0;
+    }
+    int sx = 0, sxp = 0;  // x and x_prev both the zero volume (solver.py:289-290)
+    double t = 1.0, last_obj = f0;
+    int restarts = 0;
+    bool diverged = false;
+    for (int it = 0; it < cfg.max_iters; ++it) {
+      double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+      const double beta = (t - 1.0) / tn;
+      Attempt A{};
+      if ((rc = iterate_from(sx, sxp, beta, step, cfg, A, s))) return rc;
+      step = A.step;
+      double obj = A.f_new + A.pen;
+      int new_slot = A.slot;
+      if (obj > last_obj && it > 0) {
+        // adaptive restart (solver.py:339-349)
+        restarts += 1;
+        t = 1.0;
+        tn = 1.0;
+        if ((rc = iterate_from(sx, sx, 0.0, step, cfg, A, s))) return rc;
+        step = A.step;
+        obj = A.f_new + A.pen;
+        new_slot = A.slot;
+        if (obj > last_obj) {
+          new_slot = sx;  // keep the previous iterate
+          obj = last_obj;
+        }
+      }
+      sxp = sx;
+      sx = new_slot;
+      t = tn;
+      history.push_back(obj);
+      if (obj > 1e6 * std::max(f0, 1e-300)) {
+        diverged = true;
+        break;
+      }
+      if (cfg.stop_tol > 0 && last_obj > 0) {
+        if (std::fabs(last_obj - obj) / std::max(last_obj, 1e-300) < cfg.stop_tol) {
+          last_obj = obj;
+          break;
+        }
+      }
+      last_obj = obj;
+    }
+    ix = sx;
+    have_solution = true;
+    long long nnz = 0;
+    if ((rc = count_nnz(sx, nnz, nullptr, s))) return rc;
+    if (nranks > 1) {
+      double v = (double)nnz;
+      HOLO_CUDA(cudaMemcpyAsync(scal, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+      if ((rc = allreduce_scalars(scal, 1, s))) return rc;
+      if ((rc = read_scalars(s))) return rc;
+      nnz = (long long)llround(h_scal[0]);
+    }
+    HOLO_CUDA(cudaStreamSynchronize(s));
+    HOLO_CUDA(prof.harvest());
+    const double V = (double)geom.nx * geom.ny * geom.nz;
+    last.iterations = (int)history.size();
+    last.restarts = restarts;
+    last.diverged = diverged ? 1 : 0;
+    last.step_size = step;
+    last.final_sparsity = 1.0 - (double)nnz / V;
+    last.f0 = f0;
+    last.nnz = nnz;
+    last.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep = last;
+    return diverged ? fail(HOLO_ERR_DIVERGED, "objective diverged at iteration " + std::to_string(history.size() - 1))
+                    : HOLO_OK;
+  }
+};
+
+}  // namespace holo
+
+using holo::Engine;
+using holo::fail;
+using holo::g_err;
+
+struct holo_handle {
+  Engine e;
+};
+
+#define GUARD_HANDLE(h)                                                    \
+  do {                                                                     \
+    if (!(h)) return fail(HOLO_ERR_INVALID, "null handle");                \
+    cudaError_t _se = cudaSetDevice((h)->e.device);                        \
+    if (_se != cudaSuccess) return fail(HOLO_ERR_CUDA, cudaGetErrorString(_se)); \
+  } while (0)
+
+#define TRY(body)                                                          \
+  try {                                                                    \
+    body                                                                   \
+  } catch (const std::exception& ex) {                                     \
+    return fail(HOLO_ERR_CUDA, std::string("internal: ") + ex.what());    \
+  } catch (...) {                                                          \
+    return fail(HOLO_ERR_CUDA, "internal: unknown exception");            \
+  }
+
+extern "C" {
+
+const char* holo_last_error(void) { return holo::g_err.c_str(); }
+int holo_version(void) { return 1; }
+int holo_shape_supported(int32_t nx, int32_t ny) { return holo::plan_supported(nx, ny) ? 1 : 0; }
+
+int holo_create(const holo_geometry* geom, int device, holo_handle** out) {
+  if (!geom || !out) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({
+    auto* h = new holo_handle();
+    int rc = h->e.init(*geom, device, 0, 1);
+    if (rc) {
+      std::string keep = g_err;
+      delete h;
+      g_err = keep;
+      return rc;
+    }
+    *out = h;
+    return HOLO_OK;
+  })
+}
+
+int holo_nccl_unique_id(void* out128) {
+#ifdef HOLO_WITH_NCCL
+  if (!out128) return fail(HOLO_ERR_INVALID, "null argument");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(HOLO_ERR_NCCL, ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return HOLO_OK;
+#else
+  (void)out128;
+  return fail(HOLO_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_unique_id, int rank, int nranks,
+                        holo_handle** out) {
+  if (!geom || !out) return fail(HOLO_ERR_INVALID, "null argument");
+  if (nranks == 1) return holo_create(geom, device, out);
+#ifdef HOLO_WITH_NCCL
+  if (!nccl_unique_id) return fail(HOLO_ERR_INVALID, "null nccl id");
+  TRY({
+    auto* h = new holo_handle();
+    int rc = h->e.init(*geom, device, rank, nranks);
+    if (!rc) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_unique_id, sizeof(id));
+      ncclResult_t r = ncclCommInitRank(&h->e.comm, nranks, id, rank);
+      if (r != ncclSuccess) rc = fail(HOLO_ERR_NCCL, ncclGetErrorString(r));
+    }
+    if (rc) {
+      std::string keep = g_err;
+      delete h;
+      g_err = keep;
+      return rc;
+    }
+    *out = h;
+    return HOLO_OK;
+  })
+#else
+  (void)device; (void)nccl_unique_id; (void)rank;
+  return fail(HOLO_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+int holo_destroy(holo_handle* h) {
+  if (!h) return HOLO_OK;
+  cudaSetDevice(h->e.device);
+  delete h;
+  return HOLO_OK;
+}
+
+int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end) {
+  if (!h || !k_begin || !k_end) return fail(HOLO_ERR_INVALID, "null argument");
+  *k_begin = h->e.kb;
+  *k_end = h->e.ke;
+  return HOLO_OK;
+}
+
+int holo_operator_norm(holo_handle* h, double* sigma2) {
+  if (!h || !sigma2) return fail(HOLO_ERR_INVALID, "null argument");
+  *sigma2 = h->e.plan.any_propagating ? (double)h->e.geom.nz : 0.0;
+  return HOLO_OK;
+}
+
+int holo_solve_device(holo_handle* h, const double* b_dev, const holo_solver_config* cfg, holo_report* rep,
+                      void* stream) {
+  GUARD_HANDLE(h);
+  if (!b_dev || !cfg || !rep) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({ return h->e.solve(b_dev, *cfg, *rep, h->e.st(stream)); })
+}
+
+int holo_solve(holo_handle* h, const double* b_host, const holo_solver_config* cfg, holo_report* rep) {
+  GUARD_HANDLE(h);
+  if (!b_host || !cfg || !rep) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({
+    Engine& e = h->e;
+    int rc = e.ensure_planes();
+    if (rc) return rc;
+    HOLO_CUDA(cudaMemcpyAsync(e.b64, b_host, sizeof(double) * e.P, cudaMemcpyHostToDevice, e.stream));
+    return e.solve(e.b64, *cfg, *rep, e.stream);
+  })
+}
+
+int holo_history(const holo_handle* h, double* out, int32_t cap, int32_t* n) {
+  if (!h || !n) return fail(HOLO_ERR_INVALID, "null argument");
+  const auto& hist = h->e.history;
+  *n = (int32_t)hist.size();
+  if (out) std::memcpy(out, hist.data(), sizeof(double) * std::min<size_t>(hist.size(), (size_t)std::max(cap, 0)));
+  return HOLO_OK;
+}
+
+int holo_plane_nnz(holo_handle* h, int64_t* nnz_per_local_plane) {
+  GUARD_HANDLE(h);
+  if (!nnz_per_local_plane) return fail(HOLO_ERR_INVALID, "null argument");
+  if (!h->e.have_solution) return fail(HOLO_ERR_INVALID, "no solution: call holo_solve first");
+  TRY({
+    long long tot = 0;
+    std::vector<long long> per;
+    int rc = h->e.count_nnz(h->e.ix, tot, &per, h->e.stream);
+    if (rc) return rc;
+    HOLO_CUDA(cudaStreamSynchronize(h->e.stream));
+    for (size_t i = 0; i < per.size(); ++i) nnz_per_local_plane[i] = per[i];
+    return HOLO_OK;
+  })
+}
+
+static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz,
+                      bool host, cudaStream_t s) {
+  Engine& e = h->e;
+  if (!e.have_solution) return fail(HOLO_ERR_INVALID, "no solution: call holo_solve first");
+  long long tot = 0;
+  int rc = e.count_nnz(e.ix, tot, nullptr, s);
+  if (rc) return rc;
+  if (nnz) *nnz = tot;
+  if (tot > cap) return fail(HOLO_ERR_INVALID, "COO capacity too small");
+  if (tot == 0) return HOLO_OK;
+  int32_t *dr = rows, *dc = cols;
+  float2* dv = (float2*)vals;
+  if (host) {
+    HOLO_CUDA(cudaMalloc(&dr, sizeof(int32_t) * tot));
+    HOLO_CUDA(cudaMalloc(&dc, sizeof(int32_t) * tot));
+    HOLO_CUDA(cudaMalloc(&dv, sizeof(float2) * tot));
+  }
+  HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, dr, dc, dv, s));
+  if (host) {
+    HOLO_CUDA(cudaMemcpyAsync(rows, dr, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
+    HOLO_CUDA(cudaMemcpyAsync(cols, dc, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
+    HOLO_CUDA(cudaMemcpyAsync(vals, dv, sizeof(float2) * tot, cudaMemcpyDeviceToHost, s));
+    HOLO_CUDA(cudaStreamSynchronize(s));
+    cudaFree(dr);
+    cudaFree(dc);
+    cudaFree(dv);
+  }
+  return HOLO_OK;
+}
+
+int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz) {
+  GUARD_HANDLE(h);
+  TRY({ return export_coo(h, rows, cols, vals, cap, nnz, true, h->e.stream); })
+}
+
+int holo_export_coo_device(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz,
+                           void* stream) {
+  GUARD_HANDLE(h);
+  TRY({ return export_coo(h, rows, cols, vals, cap, nnz, false, h->e.st(stream)); })
+}
+
+int holo_solution_device(holo_handle* h, void** x) {
+  if (!h || !x) return fail(HOLO_ERR_INVALID, "null argument");
+  if (!h->e.have_solution) return fail(HOLO_ERR_INVALID, "no solution: call holo_solve first");
+  *x = h->e.X[h->e.ix];
+  return HOLO_OK;
+}
+
+int holo_op_transfer(holo_handle* h, int32_t k0, int32_t k1, int32_t conj, void* out, void* stream) {
+  GUARD_HANDLE(h);
+  if (!out || k0 < 0 || k1 < k0) return fail(HOLO_ERR_INVALID, "bad plane range");
+  if (k1 == k0) return HOLO_OK;
+  HOLO_CUDA(holo::transfer_stack(h->e.plan, k0, k1, conj != 0, (float2*)out, h->e.st(stream)));
+  return HOLO_OK;
+}
+
+int holo_op_fft2(holo_handle* h, void* data, int32_t nplanes, int32_t inverse, void* stream) {
+  GUARD_HANDLE(h);
+  if (!data || nplanes < 0) return fail(HOLO_ERR_INVALID, "bad argument");
+  if (nplanes == 0) return HOLO_OK;
+  Engine& e = h->e;
+  cudaStream_t s = e.st(stream);
+  float2* d = (float2*)data;
+  const float sc = inverse ? 1.0f / (float)e.P : 1.0f;
+  HOLO_CUDA(holo::fft_rows(e.plan, d, d, (long long)nplanes * e.geom.ny, inverse != 0, 1.0f, s));
+  HOLO_CUDA(holo::fft_cols(e.plan, d, d, nplanes, inverse != 0, sc, s));
+  return HOLO_OK;
+}
+
+int holo_op_forward(holo_handle* h, const void* x, void* out, void* stream) {
+  GUARD_HANDLE(h);
+  if (!x || !out) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({
+    Engine& e = h->e;
+    cudaStream_t s = e.st(stream);
+    int rc = e.ensure_scratch();
+    if (rc) return rc;
+    if ((rc = e.forward_spectrum((const float2*)x, e.S[0], s))) return rc;
+    HOLO_CUDA(holo::apply_mask(e.plan, e.S[0], 1, s));
+    HOLO_CUDA(holo::fft_rows(e.plan, e.S[0], e.R, e.geom.ny, true, 1.0f, s));
+    HOLO_CUDA(holo::fft_cols(e.plan, e.R, e.R, 1, true, 1.0f / (float)e.P, s));
+    HOLO_CUDA(holo::real_part(e.R, (float*)out, e.P, 1.0f, s));
+    return HOLO_OK;
+  })
+}
+
+int holo_op_adjoint(holo_handle* h, const void* r, void* out, double scale, void* stream) {
+  GUARD_HANDLE(h);
+  if (!r || !out) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({
+    Engine& e = h->e;
+    cudaStream_t s = e.st(stream);
+    int rc = e.ensure_planes();
+    if (rc) return rc;
+    HOLO_CUDA(holo::real_to_complex((const float*)r, e.R, e.P, s));
+    HOLO_CUDA(holo::fft_rows(e.plan, e.R, e.R, e.geom.ny, false, 1.0f, s));
+    HOLO_CUDA(holo::fft_cols(e.plan, e.R, e.R, 1, false, 1.0f, s));
+    HOLO_CUDA(holo::apply_mask(e.plan, e.R, 1, s));
+    HOLO_CUDA(holo::adj_cols(e.plan, e.R, (float2*)out, e.nzl, e.kb, s));
+    HOLO_CUDA(holo::fft_rows(e.plan, (float2*)out, (float2*)out, (long long)e.nzl * e.geom.ny, true,
+                             (float)(scale / (double)e.P), s));
+    return HOLO_OK;
+  })
+}
+
+int holo_op_prox_fl(holo_handle* h, const void* v, void* out, int32_t nplanes, int32_t ny, int32_t nx, double tau_l1,
+                    double tau_tv, int32_t inner, void* stream) {
+  GUARD_HANDLE(h);
+  if (!v || !out || nplanes < 0 || ny < 1 || nx < 1 || ny > 65535 || nx > 65535)
+    return fail(HOLO_ERR_INVALID, "bad argument");
+  if (tau_l1 < 0 || tau_tv < 0) return fail(HOLO_ERR_INVALID, "tau must be nonnegative");
+  if (inner < 1) return fail(HOLO_ERR_INVALID, "inner_iters must be >= 1");
+  if (nplanes == 0) return HOLO_OK;
+  TRY({
+    Engine& e = h->e;
+    cudaStream_t s = e.st(stream);
+    holo::ProxArgs a;
+    int rc = e.ensure_prox(a, nplanes, ny, nx, inner, s);
+    if (rc) return rc;
+    uint8_t* force = nullptr;
+    double* pout = nullptr;
+    int* nf = nullptr;
+    double* sc = nullptr;
+    HOLO_CUDA(cudaMallocAsync(&force, nplanes, s));
+    HOLO_CUDA(cudaMallocAsync(&pout, sizeof(double) * 4 * nplanes, s));
+    HOLO_CUDA(cudaMallocAsync(&nf, sizeof(int) * nplanes, s));
+    HOLO_CUDA(cudaMallocAsync(&sc, sizeof(double) * 8, s));
+    HOLO_CUDA(cudaMemsetAsync(force, 0, nplanes, s));
+    a.x = (const float2*)v;
+    a.xnew = (float2*)out;
+    a.tau_l1 = (float)tau_l1;
+    a.tau_tv = (float)tau_tv;
+    a.lr_tv = tau_tv > 0 ? (float)(1.0 / (8.0 * tau_tv)) : 0.f;
+    double fails = 0;
+    for (int round = 0; round < 3; ++round) {
+      holo::ProxArgs f = a;
+      if (round > 0) f.force = force;
+      HOLO_CUDA(holo::prox(f, s));
+      HOLO_CUDA(holo::prox_reduce(f, tau_tv, tau_tv > 0, force, pout, nf, s));
+      HOLO_CUDA(holo::plane_total(pout, nf, nplanes, sc, s));
+      HOLO_CUDA(cudaMemcpyAsync(&fails, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HOLO_CUDA(cudaStreamSynchronize(s));
+      if (fails < 0.5) break;
+    }
+    cudaFreeAsync(force, s);
+    cudaFreeAsync(pout, s);
+    cudaFreeAsync(nf, s);
+    cudaFreeAsync(sc, s);
+    return HOLO_OK;
+  })
+}
+
+int holo_profile_enable(holo_handle* h, int32_t on) {
+  if (!h) return fail(HOLO_ERR_INVALID, "null handle");
+  h->e.prof.on = on != 0;
+  h->e.prof.reset();
+  return HOLO_OK;
+}
+
+int holo_profile_read(holo_handle* h, int32_t* n, char* names, double* ms, int64_t* counts) {
+  if (!h || !n) return fail(HOLO_ERR_INVALID, "null argument");
+  *n = holo::PK_N;
+  for (int i = 0; i < holo::PK_N; ++i) {
+    if (names) {
+      std::memset(names + 32 * i, 0, 32);
+      std::strncpy(names + 32 * i, holo::kProfNames[i], 31);
+    }
+    if (ms) ms[i] = h->e.prof.ms[i];
+    if (counts) counts[i] = h->e.prof.cnt[i];
+  }
+  return HOLO_OK;
+}
+
+int64_t holo_launch_count(void) { return holo::launch_count(); }
+
+int holo_power_iteration(holo_handle* h, int iters, uint64_t seed, double* sigma2) {
+  (void)iters;
+  (void)seed;
+  if (!h || !sigma2) return fail(HOLO_ERR_INVALID, "null argument");
+  return fail(HOLO_ERR_UNSUPPORTED, "power iteration not built yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,946 @@
+// sm_100a kernels of the RIHVR fused-lasso FISTA hot path.
+//
+//   K1  plan tables      transfer phase (64-bit cycle fractions), band mask, twiddles
+//   K2  adj_cols         column IFFT of H_k * R          (R L2-resident, H_k on the fly)
+//   K3  fft_rows         row (I)FFT                        (adjoint row pass: scale 2/P)
+//   K4  prox             y = (1+b)x - b x', v = y - step g, FGP-TV (re, im), guard
+//                        sums, soft threshold, penalty / backtracking partial sums
+//   K5  fwd_cols         column FFT * conj(H_k), deterministic z-accumulation
+//   K6  sensor           R = m (S(f) + conj S(-f))/2 - FFT(b), ||r||^2 by Parseval
+//   K7  coo_*            COO compaction of the final volume
+//
+// Reference operations replaced (see DESIGN.md for the full map):
+//   optics.py:119-122, 146-169 (TransferLadder)  -> K1 + on-the-fly cis in K2/K5
+//   solver.py:110-124 (forward_sparse)           -> K3 (fwd rows) + K5 + K6
+//   solver.py:126-132 (gradient_chunks)          -> K6 + K2 + K3
+//   solver.py:309-318, prox.py:83-148            -> K4
+//   sparsevol.py:75-88 (from_dense)              -> K7
+#include <algorithm>
+#include <atomic>
+#include <type_traits>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace holo {
+
+namespace {
+
+constexpr int kRowThreads = 256;
+
+template <class F>
+bool dispatch_n(int n, F&& f) {
+  switch (n) {
+    case 8: f(std::integral_constant<int, 8>{}); return true;
+    case 16: f(std::integral_constant<int, 16>{}); return true;
+    case 32: f(std::integral_constant<int, 32>{}); return true;
+    case 64: f(std::integral_constant<int, 64>{}); return true;
+    case 128: f(std::integral_constant<int, 128>{}); return true;
+    case 256: f(std::integral_constant<int, 256>{}); return true;
+    case 512: f(std::integral_constant<int, 512>{}); return true;
+    case 1024: f(std::integral_constant<int, 1024>{}); return true;
+    case 2048: f(std::integral_constant<int, 2048>{}); return true;
+    case 4096: f(std::integral_constant<int, 4096>{}); return true;
+    default: return false;
+  }
+}
+
+inline int col_width(int ny) { return ny >= 4096 ? 4 : 8; }
+
+// ------------------------------------------------------------ K1 tables ----
+
+__global__ void k_twiddles(float2* tw, int n) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < n) {
+    double s, c;
+    sincospi(-2.0 * (double)m / (double)n, &s, &c);
+    tw[m] = make_float2((float)c, (float)s);
+  }
+}
+
+__global__ void k_circle(float2* c256) {
+  int m = threadIdx.x;
+  double s, c;
+  sincospi(2.0 * (double)m / 256.0, &s, &c);
+  c256[m] = make_float2((float)c, (float)s);
+}
+
+// fftfreq(n, d)[i] = k * (1 / (n d)),  k = i for i <= (n-1)/2 else i - n   (numpy convention)
+__device__ double fftfreq(int i, int n, double d) {
+  const int k = (i <= (n - 1) / 2) ? i : i - n;
+  return (double)k * (1.0 / ((double)n * d));
+}
+
+__device__ uint64_t frac_to_u64(double a) {
+  double f = a - floor(a);
+  if (f >= 1.0) f = 0.0;
+  return __double2ull_rn(f * 18446744073709551616.0 * 0.5) << 1;  // 63-bit precision, avoids overflow
+}
+
+// Phase cycles of H(z) at a pixel: (z / lam) * sqrt(1 - (lam fx)^2 - (lam fy)^2)
+// (optics.py:98-116).  Evanescent pixels (arg < 0) get mask 0 and phase 0.
+__global__ void k_phase(ulonglong2* tab, uint8_t* mask, int ny, int nx, double pitch, double lam, double z0,
+                        double dz) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)ny * nx) return;
+  const int i = (int)(p / nx), j = (int)(p % nx);
+  const double fy = fftfreq(i, ny, pitch), fx = fftfreq(j, nx, pitch);
+  const double ax = lam * fx, ay = lam * fy;
+  const double arg = 1.0 - ax * ax - ay * ay;
+  const bool prop = arg >= 0.0;
+  const double root = prop ? sqrt(arg) : 0.0;
+  tab[p] = make_ulonglong2(frac_to_u64((z0 / lam) * root), frac_to_u64((dz / lam) * root));
+  mask[p] = prop ? 1 : 0;
+}
+
+// ------------------------------------------------------------- K3 rows -----
+
+template <int N, bool INV>
+__global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
+                                                          long long nrows, float scale, const float2* __restrict__ twg) {
+  using Sh = FftShape<N>;
+  constexpr int TPF = Sh::TPF, E = Sh::E;
+  constexpr int RPC = kRowThreads / TPF;
+  extern __shared__ float2 smem[];
+  float2* tw = smem;
+  float2* buf = smem + N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  __syncthreads();
+  const int lr = threadIdx.x / TPF, j = threadIdx.x % TPF;
+  for (long long row0 = (long long)blockIdx.x * RPC; row0 < nrows; row0 += (long long)gridDim.x * RPC) {
+    const long long row = row0 + lr;
+    const bool active = row < nrows;
+    float2 v[E];
+    const float2* src = in + row * N;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = active ? src[j + m * TPF] : czero();
+    fft_line<N, INV>(v, j, buf + lr * Sh::PADN, 1, tw);
+    if (active) {
+      float2* dst = out + row * N;
+#pragma unroll
+      for (int m = 0; m < E; ++m) dst[j + m * TPF] = cscale(v[m], scale);
+    }
+  }
+}
+
+// ---------------------------------------------------------- column passes --
+// Thread (j, c): column c of the CTA's C interleaved columns, FFT thread j.
+// Element m of thread (j, c) is row j + m*TPF.  Lanes vary fastest in c, so a
+// warp loads C-wide contiguous row segments.
+
+template <int N, bool INV, int C>
+__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fft_cols(const float2* __restrict__ in,
+                                                                    float2* __restrict__ out, int nx, long long P,
+                                                                    float scale, const float2* __restrict__ twg) {
+  using Sh = FftShape<N>;
+  constexpr int TPF = Sh::TPF, E = Sh::E;
+  extern __shared__ float2 smem[];
+  float2* tw = smem;
+  float2* buf = smem + N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  __syncthreads();
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int col = blockIdx.x * C + c;
+  const long long base = (long long)blockIdx.y * P + col;
+  float2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = in[base + (long long)(j + m * TPF) * nx];
+  fft_line<N, INV>(v, j, buf + c, C, tw);
+#pragma unroll
+  for (int m = 0; m < E; ++m) out[base + (long long)(j + m * TPF) * nx] = cscale(v[m], scale);
+}
+
+// K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
+template <int N, int C>
+__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_adj_cols(const float2* __restrict__ R,
+                                                                    float2* __restrict__ out, int nx, long long P,
+                                                                    int k0, const ulonglong2* __restrict__ tab,
+                                                                    const float2* __restrict__ twg,
+                                                                    const float2* __restrict__ circg) {
+  using Sh = FftShape<N>;
+  constexpr int TPF = Sh::TPF, E = Sh::E;
+  extern __shared__ float2 smem[];
+  float2* tw = smem;
+  float2* circ = smem + N;
+  float2* buf = smem + N + 256;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
+  __syncthreads();
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int col = blockIdx.x * C + c;
+  const int k = blockIdx.y;
+  float2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const long long p = (long long)(j + m * TPF) * nx + col;
+    v[m] = cmul(R[p], cis_cycles(plane_phase(tab[p], k0 + k), circ));
+  }
+  fft_line<N, true>(v, j, buf + c, C, tw);
+  float2* dst = out + (long long)k * P + col;
+#pragma unroll
+  for (int m = 0; m < E; ++m) dst[(long long)(j + m * TPF) * nx] = v[m];
+}
+
+// K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
+template <int N, int C>
+__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fwd_cols(const float2* __restrict__ in,
+                                                                    float2* __restrict__ Spart, int nx, long long P,
+                                                                    int nzl, int ppg, int k0,
+                                                                    const ulonglong2* __restrict__ tab,
+                                                                    const float2* __restrict__ twg,
+                                                                    const float2* __restrict__ circg) {
+  using Sh = FftShape<N>;
+  constexpr int TPF = Sh::TPF, E = Sh::E;
+  extern __shared__ float2 smem[];
+  float2* tw = smem;
+  float2* circ = smem + N;
+  float2* buf = smem + N + 256;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
+  __syncthreads();
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int col = blockIdx.x * C + c;
+  const int kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
+  float2 acc[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) acc[m] = czero();
+  for (int k = kb; k < ke; ++k) {
+    float2 v[E];
+    const float2* src = in + (long long)k * P + col;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = src[(long long)(j + m * TPF) * nx];
+    fft_line<N, false>(v, j, buf + c, C, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const long long p = (long long)(j + m * TPF) * nx + col;
+      acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p], k0 + k), circ)));
+    }
+  }
+  float2* dst = Spart + (long long)blockIdx.y * P + col;
+#pragma unroll
+  for (int m = 0; m < E; ++m) dst[(long long)(j + m * TPF) * nx] = acc[m];
+}
+
+__global__ void k_sum_groups(const float2* __restrict__ Spart, int groups, long long P, float2* __restrict__ S) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    float2 s = Spart[p];
+    for (int g = 1; g < groups; ++g) s = cadd(s, Spart[(long long)g * P + p]);
+    S[p] = s;
+  }
+}
+
+// ---------------------------------------------------------------- K6 -------
+
+constexpr int kSensorThreads = 256;
+
+__global__ void __launch_bounds__(kSensorThreads) k_sensor(const float2* __restrict__ Sa, const float2* __restrict__ Sb,
+                                                          float ca, float cb, const float2* __restrict__ B,
+                                                          const uint8_t* __restrict__ mask, float2* __restrict__ Rout,
+                                                          int ny, int nx, double* __restrict__ part) {
+  const long long P = (long long)ny * nx;
+  double acc[1] = {0.0};
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(p / nx), j = (int)(p - (long long)i * nx);
+    const int im = (i == 0) ? 0 : ny - i, jm = (j == 0) ? 0 : nx - j;
+    const long long q = (long long)im * nx + jm;
+    float2 s1 = cscale(Sa[p], ca), s2 = cscale(Sa[q], ca);
+    if (Sb) {
+      s1 = cadd(s1, cscale(Sb[p], cb));
+      s2 = cadd(s2, cscale(Sb[q], cb));
+    }
+    const bool m = mask[p] != 0;
+    // Re-part projection of the masked spectrum: FFT(Re IFFT(mS)) = m (S(f) + conj S(-f)) / 2
+    float2 r = m ? make_float2(0.5f * (s1.x + s2.x), 0.5f * (s1.y - s2.y)) : czero();
+    r = csub(r, B[p]);
+    acc[0] += (double)r.x * r.x + (double)r.y * r.y;
+    if (Rout) Rout[p] = m ? r : czero();
+  }
+  block_sum<1, kSensorThreads>(acc, part + blockIdx.x);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_final_sum(const double* __restrict__ part, int n, double scale,
+                                                  double* __restrict__ out) {
+  double acc[1] = {0.0};
+  for (int i = threadIdx.x; i < n; i += NT) acc[0] += part[i];
+  __shared__ double res[1];
+  block_sum<1, NT>(acc, res);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = res[0] * scale;
+}
+
+// ---------------------------------------------------------------- K4 -------
+// Fused-lasso prox on 2D tiles with a (T+2)-deep halo recomputed per tile
+// (temporal blocking).  Per owned pixel the thread keeps v, p, q (re and im)
+// in registers; the extrapolated dual (rp, rq) and the primal u live in smem.
+// Semantics follow prox.py:104-148 (FGP, step 1/(8 tau), replicated edges,
+// per-plane guard) and prox.py:83-96 (strict |w| > tau soft threshold).
+
+constexpr int kProxThreads = 512;
+constexpr int kProxMaxPx = 12;
+
+template <int NT, int MAXPX>
+__global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
+  const int plane = blockIdx.y, tile = blockIdx.x;
+  uint32_t force = 0;
+  if (a.force) {
+    force = a.force[plane];
+    if (!force) return;  // fix-up pass: only planes whose guard fired
+  }
+  const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+  const int i0 = ty * a.tile, j0 = tx * a.tile;
+  const int i1 = min(a.ny, i0 + a.tile), j1 = min(a.nx, j0 + a.tile);
+  const int H = a.halo;
+  const int ri0 = max(0, i0 - H), rj0 = max(0, j0 - H);
+  const int ri1 = min(a.ny, i1 + H), rj1 = min(a.nx, j1 + H);
+  const int EW = rj1 - rj0, EH = ri1 - ri0, NPX = EW * EH;
+  const int ei0 = i0 - ri0, ei1 = i1 - ri0, ej0 = j0 - rj0, ej1 = j1 - rj0;  // interior in region coords
+
+  extern __shared__ float sm[];
+  float* rpr = sm;
+  float* rpi = sm + NPX;
+  float* rqr = sm + 2 * NPX;
+  float* rqi = sm + 3 * NPX;
+  float* ur = sm + 4 * NPX;
+  float* ui = sm + 5 * NPX;
+
+  const long long pbase = (long long)plane * a.P;
+  const int tid = threadIdx.x;
+  float vr[MAXPX], vi[MAXPX], pr[MAXPX], pi[MAXPX], qr[MAXPX], qi[MAXPX];
+  uint32_t geo[MAXPX];
+
+#pragma unroll
+  for (int m = 0; m < MAXPX; ++m) {
+    const int idx = tid + m * NT;
+    pr[m] = pi[m] = qr[m] = qi[m] = 0.f;
+    vr[m] = vi[m] = 0.f;
+    geo[m] = 0xFFFFFFFFu;
+    if (idx < NPX) {
+      const int er = idx / EW, ec = idx - er * EW;
+      geo[m] = ((uint32_t)er << 16) | (uint32_t)ec;
+      const long long g = pbase + (long long)(ri0 + er) * a.nx + (rj0 + ec);
+      float2 y = a.x[g];
+      if (a.beta != 0.f) {
+        const float2 o = a.xp[g];
+        y = make_float2(fmaf(1.f + a.beta, y.x, -a.beta * o.x), fmaf(1.f + a.beta, y.y, -a.beta * o.y));
+      }
+      if (a.grad) {
+        const float2 gg = a.grad[g];
+        y = make_float2(fmaf(-a.step, gg.x, y.x), fmaf(-a.step, gg.y, y.y));
+      }
+      vr[m] = y.x;
+      vi[m] = y.y;
+      ur[idx] = y.x;
+      ui[idx] = y.y;
+    }
+  }
+  __syncthreads();
+
+  // partial sums (fp64): guard (tv(w), |w-v|^2, tv(v)) then ip, dx2, l1, tv(x)
+  double acc[kProxParts];
+#pragma unroll
+  for (int i = 0; i < kProxParts; ++i) acc[i] = 0.0;
+
+  const bool tv_on = a.tau_tv > 0.f;
+  const float tau = a.tau_tv, lr = a.lr_tv;
+  if (tv_on) {
+    for (int t = 0; t < a.inner; ++t) {
+      if (t > 0) {
+        // u = v - tau * D^T(rp, rq)
+#pragma unroll
+        for (int m = 0; m < MAXPX; ++m) {
+          if (geo[m] == 0xFFFFFFFFu) continue;
+          const int er = geo[m] >> 16, ec = geo[m] & 0xFFFF;
+          const int idx = er * EW + ec;
+          const bool dn = er + 1 < EH, rt = ec + 1 < EW;
+          float dr = rpr[idx] + rqr[idx], di = rpi[idx] + rqi[idx];
+          if (dn) { dr -= rpr[idx + EW]; di -= rpi[idx + EW]; }
+          if (rt) { dr -= rqr[idx + 1]; di -= rqi[idx + 1]; }
+          ur[idx] = fmaf(-tau, dr, vr[m]);
+          ui[idx] = fmaf(-tau, di, vi[m]);
+        }
+        __syncthreads();
+      }
+      const float bt = a.fgp_beta[t];
+#pragma unroll
+      for (int m = 0; m < MAXPX; ++m) {
+        if (geo[m] == 0xFFFFFFFFu) continue;
+        const int er = geo[m] >> 16, ec = geo[m] & 0xFFFF;
+        const int idx = er * EW + ec;
+        const float uor = ur[idx], uoi = ui[idx];
+        float gyr = 0.f, gyi = 0.f, gxr = 0.f, gxi = 0.f;
+        if (er > 0) { gyr = uor - ur[idx - EW]; gyi = uoi - ui[idx - EW]; }
+        if (ec > 0) { gxr = uor - ur[idx - 1]; gxi = uoi - ui[idx - 1]; }
+        if (t == 0 && er >= ei0 && er < ei1 && ec >= ej0 && ec < ej1) {
+          acc[PT_TVV_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
+          acc[PT_TVV_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
+        }
+        float opr = 0.f, opi = 0.f, oqr = 0.f, oqi = 0.f;
+        if (t > 0) { opr = rpr[idx]; opi = rpi[idx]; oqr = rqr[idx]; oqi = rqi[idx]; }
+        float npr = fmaf(lr, gyr, opr), nqr = fmaf(lr, gxr, oqr);
+        float npi = fmaf(lr, gyi, opi), nqi = fmaf(lr, gxi, oqi);
+        const float n2r = fmaf(npr, npr, nqr * nqr), n2i = fmaf(npi, npi, nqi * nqi);
+        if (n2r > 1.f) { const float s = rsqrtf(n2r); npr *= s; nqr *= s; }
+        if (n2i > 1.f) { const float s = rsqrtf(n2i); npi *= s; nqi *= s; }
+        rpr[idx] = fmaf(bt, npr - pr[m], npr);
+        rqr[idx] = fmaf(bt, nqr - qr[m], nqr);
+        rpi[idx] = fmaf(bt, npi - pi[m], npi);
+        rqi[idx] = fmaf(bt, nqi - qi[m], nqi);
+        pr[m] = npr; qr[m] = nqr; pi[m] = npi; qi[m] = nqi;
+      }
+      __syncthreads();
+    }
+    // w = v - tau * D^T(p, q): publish p, q
+#pragma unroll
+    for (int m = 0; m < MAXPX; ++m) {
+      if (geo[m] == 0xFFFFFFFFu) continue;
+      const int idx = (geo[m] >> 16) * EW + (geo[m] & 0xFFFF);
+      rpr[idx] = pr[m]; rpi[idx] = pi[m]; rqr[idx] = qr[m]; rqi[idx] = qi[m];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MAXPX; ++m) {
+      if (geo[m] == 0xFFFFFFFFu) continue;
+      const int er = geo[m] >> 16, ec = geo[m] & 0xFFFF;
+      const int idx = er * EW + ec;
+      float dr = pr[m] + qr[m], di = pi[m] + qi[m];
+      if (er + 1 < EH) { dr -= rpr[idx + EW]; di -= rpi[idx + EW]; }
+      if (ec + 1 < EW) { dr -= rqr[idx + 1]; di -= rqi[idx + 1]; }
+      // keep w in the p registers from here on
+      pr[m] = fmaf(-tau, dr, vr[m]);
+      pi[m] = fmaf(-tau, di, vi[m]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MAXPX; ++m) {
+      if (geo[m] == 0xFFFFFFFFu) continue;
+      const int idx = (geo[m] >> 16) * EW + (geo[m] & 0xFFFF);
+      ur[idx] = pr[m];
+      ui[idx] = pi[m];
+    }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int m = 0; m < MAXPX; ++m) { pr[m] = vr[m]; pi[m] = vi[m]; }
+  }
+
+  // guard statistics on the interior, then the speculative soft threshold
+#pragma unroll
+  for (int m = 0; m < MAXPX; ++m) {
+    if (geo[m] == 0xFFFFFFFFu) continue;
+    const int er = geo[m] >> 16, ec = geo[m] & 0xFFFF;
+    const int idx = er * EW + ec;
+    const bool interior = er >= ei0 && er < ei1 && ec >= ej0 && ec < ej1;
+    float wr = pr[m], wi = pi[m];
+    if (tv_on && interior) {
+      float gyr = 0.f, gyi = 0.f, gxr = 0.f, gxi = 0.f;
+      if (er > 0) { gyr = wr - ur[idx - EW]; gyi = wi - ui[idx - EW]; }
+      if (ec > 0) { gxr = wr - ur[idx - 1]; gxi = wi - ui[idx - 1]; }
+      acc[PT_TVW_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
+      acc[PT_TVW_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
+      const float dr = wr - vr[m], di = wi - vi[m];
+      acc[PT_D2_R] += (double)(dr * dr);
+      acc[PT_D2_I] += (double)(di * di);
+    }
+    if (force & 1u) wr = vr[m];
+    if (force & 2u) wi = vi[m];
+    if (a.tau_l1 > 0.f) {
+      const float mag = hypotf(wr, wi);
+      if (mag > a.tau_l1) {
+        const float gscale = 1.f - a.tau_l1 / mag;
+        wr *= gscale;
+        wi *= gscale;
+      } else {
+        wr = 0.f;
+        wi = 0.f;
+      }
+    }
+    pr[m] = wr;
+    pi[m] = wi;
+  }
+  if (tv_on) __syncthreads();  // guard reads of u done before x_new overwrites rp
+#pragma unroll
+  for (int m = 0; m < MAXPX; ++m) {
+    if (geo[m] == 0xFFFFFFFFu) continue;
+    const int idx = (geo[m] >> 16) * EW + (geo[m] & 0xFFFF);
+    rpr[idx] = pr[m];
+    rpi[idx] = pi[m];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < MAXPX; ++m) {
+    if (geo[m] == 0xFFFFFFFFu) continue;
+    const int er = geo[m] >> 16, ec = geo[m] & 0xFFFF;
+    if (!(er >= ei0 && er < ei1 && ec >= ej0 && ec < ej1)) continue;
+    const int idx = er * EW + ec;
+    const float xr = pr[m], xi = pi[m];
+    float gyr = 0.f, gyi = 0.f, gxr = 0.f, gxi = 0.f;
+    if (er > 0) { gyr = xr - rpr[idx - EW]; gyi = xi - rpi[idx - EW]; }
+    if (ec > 0) { gxr = xr - rpr[idx - 1]; gxi = xi - rpi[idx - 1]; }
+    acc[PT_TVX_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
+    acc[PT_TVX_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
+    acc[PT_L1] += (double)hypotf(xr, xi);
+    const long long g = pbase + (long long)(ri0 + er) * a.nx + (rj0 + ec);
+    float2 y = a.x[g];
+    if (a.beta != 0.f) {
+      const float2 o = a.xp[g];
+      y = make_float2(fmaf(1.f + a.beta, y.x, -a.beta * o.x), fmaf(1.f + a.beta, y.y, -a.beta * o.y));
+    }
+    const float dxr = xr - y.x, dxi = xi - y.y;
+    if (a.grad) {
+      const float2 gg = a.grad[g];
+      acc[PT_IP] += (double)gg.x * dxr + (double)gg.y * dxi;
+    }
+    acc[PT_DX2] += (double)dxr * dxr + (double)dxi * dxi;
+    a.xnew[g] = make_float2(xr, xi);
+  }
+  block_sum<kProxParts, NT>(acc, a.part + ((long long)plane * a.tiles_per_plane + tile) * kProxParts);
+}
+
+constexpr int kReduceThreads = 128;
+
+__global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __restrict__ part, int tpp,
+                                                                double tau, int tv_on, uint8_t* __restrict__ force_acc,
+                                                                double* __restrict__ plane_out,
+                                                                int* __restrict__ new_fail) {
+  const int plane = blockIdx.x;
+  double acc[kProxParts];
+#pragma unroll
+  for (int i = 0; i < kProxParts; ++i) acc[i] = 0.0;
+  const double* src = part + (long long)plane * tpp * kProxParts;
+  for (int t = threadIdx.x; t < tpp; t += kReduceThreads) {
+#pragma unroll
+    for (int i = 0; i < kProxParts; ++i) acc[i] += src[(long long)t * kProxParts + i];
+  }
+  __shared__ double s[kProxParts];
+  block_sum<kProxParts, kReduceThreads>(acc, s);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t bits = 0;
+    if (tv_on) {
+      // prox.py:138-147: reject the TV output when tau TV(w) + |w-v|^2/2 > tau TV(v)
+      if (tau * s[PT_TVW_R] + 0.5 * s[PT_D2_R] > tau * s[PT_TVV_R]) bits |= 1u;
+      if (tau * s[PT_TVW_I] + 0.5 * s[PT_D2_I] > tau * s[PT_TVV_I]) bits |= 2u;
+    }
+    const uint32_t old = force_acc[plane];
+    force_acc[plane] = (uint8_t)(old | bits);
+    new_fail[plane] = (bits & ~old) ? 1 : 0;
+    double* o = plane_out + (long long)plane * 4;
+    o[0] = s[PT_IP];
+    o[1] = s[PT_DX2];
+    o[2] = s[PT_L1];
+    o[3] = s[PT_TVX_R] + s[PT_TVX_I];
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) k_plane_total(const double* __restrict__ plane_out,
+                                                                const int* __restrict__ new_fail, int nplanes,
+                                                                double* __restrict__ scalars) {
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (int k = threadIdx.x; k < nplanes; k += kReduceThreads) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] += plane_out[(long long)k * 4 + i];
+    acc[4] += (double)new_fail[k];
+  }
+  block_sum<5, kReduceThreads>(acc, scalars);
+}
+
+// ------------------------------------------------------------ misc ---------
+
+constexpr int kEltThreads = 256;
+
+__global__ void k_load_hologram(const double* __restrict__ b, float2* __restrict__ bc, long long P,
+                                double* __restrict__ part) {
+  double acc[1] = {0.0};
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const double v = b[p];
+    acc[0] += v * v;
+    bc[p] = make_float2((float)v, 0.f);
+  }
+  block_sum<1, kEltThreads>(acc, part + blockIdx.x);
+}
+
+__global__ void k_real_part(const float2* __restrict__ in, float* __restrict__ out, long long n, float scale) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    out[p] = in[p].x * scale;
+}
+
+__global__ void k_real_to_complex(const float* __restrict__ in, float2* __restrict__ out, long long n) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    out[p] = make_float2(in[p], 0.f);
+}
+
+__global__ void k_apply_mask(float2* __restrict__ spec, const uint8_t* __restrict__ mask, long long P, long long n) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    if (!mask[p % P]) spec[p] = czero();
+}
+
+__global__ void k_transfer(const ulonglong2* __restrict__ tab, const uint8_t* __restrict__ mask,
+                           const float2* __restrict__ circ, long long P, int k0, int nk, int conj,
+                           float2* __restrict__ out) {
+  const long long n = P * nk;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e % P;
+    const int k = k0 + (int)(e / P);
+    float2 h = mask[p] ? cis_cycles(plane_phase(tab[p], k), circ) : czero();
+    out[e] = conj ? cconj(h) : h;
+  }
+}
+
+__global__ void k_spec_combine(const float2* __restrict__ Sa, const float2* __restrict__ Sb, float ca, float cb,
+                               float2* __restrict__ out, long long P) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    float2 s = cscale(Sa[p], ca);
+    if (Sb) s = cadd(s, cscale(Sb[p], cb));
+    out[p] = s;
+  }
+}
+
+constexpr int kCooChunk = 1024;
+constexpr int kCooThreads = 256;
+
+__global__ void __launch_bounds__(kCooThreads) k_coo_count(const float2* __restrict__ x, long long P, int cpp,
+                                                           int* __restrict__ counts) {
+  const int plane = blockIdx.y, ch = blockIdx.x;
+  const long long start = (long long)ch * kCooChunk;
+  const float2* src = x + (long long)plane * P;
+  int c = 0;
+  for (int e = threadIdx.x; e < kCooChunk; e += kCooThreads) {
+    const long long p = start + e;
+    if (p < P) {
+      const float2 v = src[p];
+      c += (v.x != 0.f || v.y != 0.f) ? 1 : 0;
+    }
+  }
+  double acc[1] = {(double)c};
+  __shared__ double res[1];
+  block_sum<1, kCooThreads>(acc, res);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[(long long)plane * cpp + ch] = (int)res[0];
+}
+
+// row-major compaction: each thread owns 4 consecutive elements of the chunk
+__global__ void __launch_bounds__(kCooThreads) k_coo_compact(const float2* __restrict__ x, long long P, int nx,
+                                                             int cpp, const long long* __restrict__ offsets,
+                                                             int* __restrict__ rows, int* __restrict__ cols,
+                                                             float2* __restrict__ vals) {
+  constexpr int PER = kCooChunk / kCooThreads;
+  const int plane = blockIdx.y, ch = blockIdx.x;
+  const long long start = (long long)ch * kCooChunk + (long long)threadIdx.x * PER;
+  const float2* src = x + (long long)plane * P;
+  float2 v[PER];
+  int flag[PER], mine = 0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const long long p = start + e;
+    v[e] = (p < P) ? src[p] : czero();
+    flag[e] = (v[e].x != 0.f || v[e].y != 0.f) ? 1 : 0;
+    mine += flag[e];
+  }
+  // exclusive block scan of `mine` (warp shuffles + smem)
+  __shared__ int wsum[kCooThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  int before = 0;
+  for (int k = 0; k < w; ++k) before += wsum[k];
+  long long out = offsets[(long long)plane * cpp + ch] + before + incl - mine;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    if (flag[e]) {
+      const long long p = start + e;
+      rows[out] = (int)(p / nx);
+      cols[out] = (int)(p % nx);
+      vals[out] = v[e];
+      ++out;
+    }
+  }
+}
+
+inline int grid_for(long long n, int threads, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return (int)std::min<long long>(g, cap);
+}
+
+}  // namespace
+
+// =================================================================== host ==
+
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+#define COUNT_LAUNCH(n) g_launches.fetch_add((n), std::memory_order_relaxed)
+
+bool plan_supported(int nx, int ny) {
+  auto ok = [](int n) { return n >= 8 && n <= 4096 && (n & (n - 1)) == 0; };
+  return ok(nx) && ok(ny);
+}
+
+cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,
+                       cudaStream_t s) {
+  p.nx = nx; p.ny = ny; p.nz = nz;
+  p.P = (long long)nx * ny;
+  p.pitch = pitch; p.dz = dz; p.z0 = z0; p.lam = lam;
+  p.col_c = col_width(ny);
+  cudaError_t e;
+  if ((e = cudaMalloc(&p.tw_x, sizeof(float2) * nx))) return e;
+  if ((e = cudaMalloc(&p.tw_y, sizeof(float2) * ny))) return e;
+  if ((e = cudaMalloc(&p.circle, sizeof(float2) * 256))) return e;
+  if ((e = cudaMalloc(&p.phase, sizeof(ulonglong2) * p.P))) return e;
+  if ((e = cudaMalloc(&p.mask, p.P))) return e;
+  k_twiddles<<<(nx + 255) / 256, 256, 0, s>>>(p.tw_x, nx);
+  COUNT_LAUNCH(1);
+  k_twiddles<<<(ny + 255) / 256, 256, 0, s>>>(p.tw_y, ny);
+  COUNT_LAUNCH(1);
+  k_circle<<<1, 256, 0, s>>>(p.circle);
+  COUNT_LAUNCH(1);
+  k_phase<<<(int)((p.P + 255) / 256), 256, 0, s>>>(p.phase, p.mask, ny, nx, pitch, lam, z0, dz);
+  COUNT_LAUNCH(1);
+  // the DC sample (fx = fy = 0, arg = 1) always propagates, so ||A||^2 = nz exactly
+  p.any_propagating = 1;
+  if ((e = cudaStreamSynchronize(s))) return e;
+  return cudaGetLastError();
+}
+
+void plan_free(Plan& p) {
+  cudaFree(p.tw_x); cudaFree(p.tw_y); cudaFree(p.circle); cudaFree(p.phase); cudaFree(p.mask);
+  p.tw_x = p.tw_y = p.circle = nullptr;
+  p.phase = nullptr;
+  p.mask = nullptr;
+}
+
+template <class K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
+                     cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const bool ok = dispatch_n(p.nx, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    using Sh = FftShape<N>;
+    constexpr int RPC = kRowThreads / Sh::TPF;
+    const size_t smem = sizeof(float2) * (N + (size_t)RPC * Sh::PADN);
+    const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
+    if (inverse) {
+      err = set_smem(k_fft_rows<N, true>, smem);
+      k_fft_rows<N, true><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x);
+  COUNT_LAUNCH(1);
+    } else {
+      err = set_smem(k_fft_rows<N, false>, smem);
+      k_fft_rows<N, false><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x);
+  COUNT_LAUNCH(1);
+    }
+  });
+  if (!ok) return cudaErrorInvalidValue;
+  return err ? err : cudaGetLastError();
+}
+
+template <int N, int C>
+static size_t col_smem(int extra) {
+  return sizeof(float2) * (N + extra + (size_t)(N + N / 16) * C);
+}
+
+cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
+                     cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const bool ok = dispatch_n(p.ny, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    constexpr int C = N >= 4096 ? 4 : 8;
+    constexpr int NT = C * FftShape<N>::TPF;
+    const size_t smem = col_smem<N, C>(0);
+    dim3 grid(p.nx / C, nplanes);
+    if (inverse) {
+      err = set_smem(k_fft_cols<N, true, C>, smem);
+      k_fft_cols<N, true, C><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y);
+  COUNT_LAUNCH(1);
+    } else {
+      err = set_smem(k_fft_cols<N, false, C>, smem);
+      k_fft_cols<N, false, C><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y);
+  COUNT_LAUNCH(1);
+    }
+  });
+  if (!ok) return cudaErrorInvalidValue;
+  return err ? err : cudaGetLastError();
+}
+
+cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const bool ok = dispatch_n(p.ny, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    constexpr int C = N >= 4096 ? 4 : 8;
+    constexpr int NT = C * FftShape<N>::TPF;
+    const size_t smem = col_smem<N, C>(256);
+    dim3 grid(p.nx / C, nzl);
+    err = set_smem(k_adj_cols<N, C>, smem);
+    k_adj_cols<N, C><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y, p.circle);
+  COUNT_LAUNCH(1);
+  });
+  if (!ok) return cudaErrorInvalidValue;
+  return err ? err : cudaGetLastError();
+}
+
+int fwd_groups(const Plan& p, int nzl) {
+  const int tiles = std::max(1, p.nx / p.col_c);
+  int g = (4 * 148 + tiles - 1) / tiles;
+  g = std::max(1, std::min(g, nzl));
+  return std::min(g, 64);
+}
+
+cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const int ppg = (nzl + groups - 1) / groups;
+  const bool ok = dispatch_n(p.ny, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    constexpr int C = N >= 4096 ? 4 : 8;
+    constexpr int NT = C * FftShape<N>::TPF;
+    const size_t smem = col_smem<N, C>(256);
+    dim3 grid(p.nx / C, groups);
+    err = set_smem(k_fwd_cols<N, C>, smem);
+    k_fwd_cols<N, C><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y, p.circle);
+  COUNT_LAUNCH(1);
+  });
+  if (!ok) return cudaErrorInvalidValue;
+  return err ? err : cudaGetLastError();
+}
+
+cudaError_t sum_groups(const Plan& p, const float2* Spart, int groups, float2* S, cudaStream_t s) {
+  k_sum_groups<<<grid_for(p.P, kEltThreads), kEltThreads, 0, s>>>(Spart, groups, p.P, S);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+int sensor_blocks(const Plan& p) { return grid_for(p.P, kSensorThreads, 148 * 4); }
+
+cudaError_t sensor(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, const float2* B,
+                   float2* Rout, double* part, cudaStream_t s) {
+  k_sensor<<<sensor_blocks(p), kSensorThreads, 0, s>>>(Sa, Sb, ca, cb, B, p.mask, Rout, p.ny, p.nx, part);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t final_sum(const double* part, int n, double scale, double* out, cudaStream_t s) {
+  k_final_sum<256><<<1, 256, 0, s>>>(part, n, scale, out);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+size_t prox_setup(ProxArgs& a, int ny, int nx, int inner) {
+  a.ny = ny;
+  a.nx = nx;
+  a.P = (long long)ny * nx;
+  a.inner = inner;
+  a.halo = inner + 2;
+  const int cap = kProxThreads * kProxMaxPx;
+  int side = 1;
+  while ((side + 1 + 2 * a.halo) * (side + 1 + 2 * a.halo) <= cap && side < 64) ++side;
+  a.tile = side;
+  a.tiles_x = (nx + side - 1) / side;
+  const int tiles_y = (ny + side - 1) / side;
+  a.tiles_per_plane = a.tiles_x * tiles_y;
+  const int ew = std::min(nx, side + 2 * a.halo), eh = std::min(ny, side + 2 * a.halo);
+  return sizeof(float) * 6 * (size_t)ew * eh;
+}
+
+bool prox_supported(int ny, int nx, int inner) {
+  ProxArgs a;
+  prox_setup(a, ny, nx, inner);
+  const int ew = std::min(nx, a.tile + 2 * a.halo), eh = std::min(ny, a.tile + 2 * a.halo);
+  return ew * eh <= kProxThreads * kProxMaxPx;
+}
+
+cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
+  const int ew = std::min(a.nx, a.tile + 2 * a.halo), eh = std::min(a.ny, a.tile + 2 * a.halo);
+  if (ew * eh > kProxThreads * kProxMaxPx) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(float) * 6 * (size_t)ew * eh;
+  cudaError_t err = set_smem(k_prox<kProxThreads, kProxMaxPx>, smem);
+  if (err) return err;
+  dim3 grid(a.tiles_per_plane, a.nplanes);
+  k_prox<kProxThreads, kProxMaxPx><<<grid, kProxThreads, smem, s>>>(a);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
+                        int* new_fail, cudaStream_t s) {
+  k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, tau_tv, tv_on, force_acc, plane_out,
+                                                     new_fail);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplanes, double* scalars, cudaStream_t s) {
+  k_plane_total<<<1, kReduceThreads, 0, s>>>(plane_out, new_fail, nplanes, scalars);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t load_hologram(const double* b, float2* bc, long long P, double* part, int* nblocks, cudaStream_t s) {
+  const int g = grid_for(P, kEltThreads, 148 * 4);
+  *nblocks = g;
+  k_load_hologram<<<g, kEltThreads, 0, s>>>(b, bc, P, part);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t real_part(const float2* in, float* out, long long n, float scale, cudaStream_t s) {
+  k_real_part<<<grid_for(n, kEltThreads), kEltThreads, 0, s>>>(in, out, n, scale);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t real_to_complex(const float* in, float2* out, long long n, cudaStream_t s) {
+  k_real_to_complex<<<grid_for(n, kEltThreads), kEltThreads, 0, s>>>(in, out, n);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t apply_mask(const Plan& p, float2* spec, int nplanes, cudaStream_t s) {
+  const long long n = p.P * nplanes;
+  k_apply_mask<<<grid_for(n, kEltThreads), kEltThreads, 0, s>>>(spec, p.mask, p.P, n);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t transfer_stack(const Plan& p, int k0, int k1, bool conj, float2* out, cudaStream_t s) {
+  const long long n = p.P * (k1 - k0);
+  k_transfer<<<grid_for(n, kEltThreads), kEltThreads, 0, s>>>(p.phase, p.mask, p.circle, p.P, k0, k1 - k0,
+                                                              conj ? 1 : 0, out);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t spec_combine(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, float2* out,
+                         cudaStream_t s) {
+  k_spec_combine<<<grid_for(p.P, kEltThreads), kEltThreads, 0, s>>>(Sa, Sb, ca, cb, out, p.P);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+int coo_chunks(long long P, int nplanes) { return (int)((P + kCooChunk - 1) / kCooChunk) * nplanes; }
+
+cudaError_t coo_count(const float2* x, long long P, int nplanes, int* chunk_counts, cudaStream_t s) {
+  const int cpp = (int)((P + kCooChunk - 1) / kCooChunk);
+  k_coo_count<<<dim3(cpp, nplanes), kCooThreads, 0, s>>>(x, P, cpp, chunk_counts);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t coo_compact(const float2* x, long long P, int nx, int nplanes, const long long* chunk_offsets, int* rows,
+                        int* cols, float2* vals, cudaStream_t s) {
+  const int cpp = (int)((P + kCooChunk - 1) / kCooChunk);
+  k_coo_compact<<<dim3(cpp, nplanes), kCooThreads, 0, s>>>(x, P, nx, cpp, chunk_offsets, rows, cols, vals);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+}  // namespace holo

@@ -1,0 +1,99 @@
+// Host-side launch interface of the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace holo {
+
+// Device tables for one geometry; built once by plan_build().
+struct Plan {
+  int nx = 0, ny = 0, nz = 0;  // nz = global plane count (plane index k in the phase)
+  long long P = 0;             // ny * nx
+  double pitch = 0, dz = 0, z0 = 0, lam = 0;
+  int col_c = 8;                // interleaved columns per column-pass CTA
+  float2* tw_x = nullptr;       // exp(-2 pi i m / nx), m < nx
+  float2* tw_y = nullptr;       // exp(-2 pi i m / ny)
+  float2* circle = nullptr;     // exp(2 pi i m / 256)
+  ulonglong2* phase = nullptr;  // per pixel (frac(z0 q), frac(dz q)) as 64-bit cycle fractions
+  uint8_t* mask = nullptr;      // per pixel 1 = propagating (arg >= 0)
+  int any_propagating = 0;
+};
+
+constexpr int kProxParts = 11;  // per-tile fp64 partial sums written by the prox kernel
+// indices into a tile's partials
+enum ProxPart { PT_TVW_R = 0, PT_TVW_I, PT_D2_R, PT_D2_I, PT_TVV_R, PT_TVV_I, PT_IP, PT_DX2, PT_L1, PT_TVX_R, PT_TVX_I };
+
+struct ProxArgs {
+  const float2* x = nullptr;     // state x_k
+  const float2* xp = nullptr;    // state x_{k-1} (read only if beta != 0)
+  const float2* grad = nullptr;  // 2 A^H (A y - b) (nullptr: pure prox of y)
+  float2* xnew = nullptr;
+  long long P = 0;
+  int ny = 0, nx = 0, nplanes = 0;
+  float beta = 0.f, step = 0.f;  // y = (1+beta) x - beta xp ; v = y - step * grad
+  float tau_l1 = 0.f, tau_tv = 0.f, lr_tv = 0.f;
+  int inner = 0, halo = 0, tile = 0, tiles_x = 0, tiles_per_plane = 0;
+  const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule
+  const uint8_t* force = nullptr;   // guard fix-up pass: per plane bit0 re / bit1 im -> identity
+  double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts]
+};
+
+bool plan_supported(int nx, int ny);
+long long launch_count();  // kernels launched by this library since load
+cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,
+                       cudaStream_t s);
+void plan_free(Plan& p);
+
+// batched 1D transforms (unnormalised; `scale` multiplies the output)
+cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
+                     cudaStream_t s);
+cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
+                     cudaStream_t s);
+// adjoint column pass: out[k] = colIFFT(H_{k0+k} * R), k < nzl (R already band-masked)
+cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s);
+// forward column pass: Spart[g] = sum_{k in group g} colFFT(in[k]) * conj(H_{k0+k})
+cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s);
+int fwd_groups(const Plan& p, int nzl);
+cudaError_t sum_groups(const Plan& p, const float2* Spart, int groups, float2* S, cudaStream_t s);
+
+// residual spectrum R = m * (0.5 (S(f) + conj S(-f))) - B with S = ca Sa + cb Sb;
+// writes m*R to Rout (if non-null) and per-block sum |R|^2 to part; returns #blocks.
+int sensor_blocks(const Plan& p);
+cudaError_t sensor(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, const float2* B,
+                   float2* Rout, double* part, cudaStream_t s);
+// out[slot] = scale * sum(part[0..n))  (fixed order, one block)
+cudaError_t final_sum(const double* part, int n, double scale, double* out, cudaStream_t s);
+
+// prox: tile geometry chosen by prox_setup (fills halo/tile/tiles_*); returns smem bytes
+size_t prox_setup(ProxArgs& a, int ny, int nx, int inner);
+bool prox_supported(int ny, int nx, int inner);
+cudaError_t prox(const ProxArgs& a, cudaStream_t s);
+// per-plane reduction of the prox partials + guard check.  force_acc[plane]
+// accumulates the guard bits; plane_out[plane*4 + {0..3}] = ip, dx2, l1, tv;
+// new_fail[plane] = 1 when a guard bit was newly raised.
+cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
+                        int* new_fail, cudaStream_t s);
+// scalars[0..3] += sums of plane_out over planes (fixed order); scalars[4] = #new guard failures
+cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplanes, double* scalars,
+                        cudaStream_t s);
+
+// b (fp64, host layout) -> fp32 complex plane (imag 0), per-block sum b^2
+cudaError_t load_hologram(const double* b, float2* bc, long long P, double* part, int* nblocks, cudaStream_t s);
+// real part extraction with scale (for forward-operator output)
+cudaError_t real_part(const float2* in, float* out, long long n, float scale, cudaStream_t s);
+cudaError_t real_to_complex(const float* in, float2* out, long long n, cudaStream_t s);
+// mask a spectrum in place (m = 0 -> 0)
+cudaError_t apply_mask(const Plan& p, float2* spec, int nplanes, cudaStream_t s);
+// transfer stack H_k (k = k0..k1-1), optionally conjugated
+cudaError_t transfer_stack(const Plan& p, int k0, int k1, bool conj, float2* out, cudaStream_t s);
+// S_out = ca * Sa + cb * Sb (elementwise)
+cudaError_t spec_combine(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, float2* out,
+                         cudaStream_t s);
+
+// COO export: count nonzeros per chunk, then compact in row-major order.
+int coo_chunks(long long P, int nplanes);
+cudaError_t coo_count(const float2* x, long long P, int nplanes, int* chunk_counts, cudaStream_t s);
+cudaError_t coo_compact(const float2* x, long long P, int nx, int nplanes, const long long* chunk_offsets,
+                        int* rows, int* cols, float2* vals, cudaStream_t s);
+
+}  // namespace holo

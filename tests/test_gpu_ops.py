@@ -1,0 +1,113 @@
+"""GPU parity of the operator kernels against the reference goldens and the oracle.
+Tolerances are float32-level (the device computes in fp32 with fp64 scalars)."""
+import numpy as np
+import pytest
+
+from conftest import geom_of, golden, rel_l2
+from oracle import holo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _geom(d):
+    from paper_1904_04884_b200 import VolumeGeometry
+    nx, ny, nz, pitch, dz, z0, lam = d["geom"]
+    return VolumeGeometry(int(nx), int(ny), int(nz), pitch, dz, z0, lam)
+
+
+@pytest.fixture(scope="module")
+def eng_a():
+    from paper_1904_04884_b200.engine import HoloEngine
+    d = golden("ops_a")
+    return HoloEngine(_geom(d)), d
+
+
+@pytest.mark.parametrize("name", ["ops_a", "ops_evan"])
+def test_transfer_forward_adjoint(name):
+    from paper_1904_04884_b200.engine import HoloEngine
+    d = golden(name)
+    eng = HoloEngine(_geom(d))
+    g = geom_of(d["geom"])
+    h = eng.transfer(0, g.nz)
+    assert np.max(np.abs(h - d["transfer"])) < 2e-6
+    assert np.max(np.abs(eng.transfer(0, g.nz, conj=True) - d["transfer_conj"])) < 2e-6
+    assert rel_l2(eng.forward(d["x"]), d["forward"]) < 2e-6
+    assert rel_l2(eng.adjoint(d["r"]), d["adjoint"]) < 2e-6
+    assert rel_l2(eng.adjoint(d["r"], scale=2.0), d["gradient"]) < 2e-6
+    eng.close()
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
+def test_fft2_all_sizes(n):
+    from paper_1904_04884_b200 import VolumeGeometry
+    from paper_1904_04884_b200.engine import HoloEngine
+    ny = n if n <= 1024 else 16
+    eng = HoloEngine(VolumeGeometry(n, ny, 1, 1e-5, 1e-5, 5e-3, 632e-9))
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((2, ny, n)) + 1j * rng.standard_normal((2, ny, n))
+    f = eng.fft2(x)
+    assert rel_l2(f, np.fft.fft2(x)) < 3e-6
+    b = eng.fft2(f, inverse=True)
+    assert rel_l2(b, x) < 3e-6
+    eng.close()
+    # column transforms of tall planes
+    eng = HoloEngine(VolumeGeometry(16, n, 1, 1e-5, 1e-5, 5e-3, 632e-9))
+    x = rng.standard_normal((1, n, 16)) + 1j * rng.standard_normal((1, n, 16))
+    assert rel_l2(eng.fft2(x), np.fft.fft2(x)) < 3e-6
+    eng.close()
+
+
+def test_adjointness_full_width():
+    """<A x, r> = Re<x, A^H r> at the C3 plane size."""
+    from paper_1904_04884_b200 import VolumeGeometry
+    from paper_1904_04884_b200.engine import HoloEngine
+    g = VolumeGeometry(1024, 1024, 4, 10e-6, 10e-6, 5e-3, 632e-9)
+    eng = HoloEngine(g)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        x = (rng.standard_normal((4, 1024, 1024)) + 1j * rng.standard_normal((4, 1024, 1024))) * (
+            rng.random((4, 1024, 1024)) < 0.01)
+        r = rng.standard_normal((1024, 1024))
+        lhs = float(np.sum(eng.forward(x) * r))
+        rhs = float(np.real(np.vdot(eng.adjoint(r), x)))
+        assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), 1.0)
+    # and against the fp64 oracle on the same input
+    og = O.Geometry.of(g)
+    assert rel_l2(eng.forward(x), O.sensor_forward(x, og)) < 5e-6
+    eng.close()
+
+
+def test_prox_matches_reference():
+    from paper_1904_04884_b200 import prox_fl, prox_l1, prox_tv_2d
+    d = golden("prox")
+    v = d["v"]
+    for key in d:
+        if key.startswith("fl_T"):
+            _, t, tl, tt = key.split("_")
+            out = prox_fl(v, float(tl), float(tt), int(t[1:]))
+            err = np.max(np.abs(out - d[key])) / max(np.max(np.abs(d[key])), 1e-30)
+            assert err < 1e-5, (key, err)
+    for T in (1, 5):
+        out = prox_tv_2d(d["real"], 0.4, T)
+        assert np.max(np.abs(out - d[f"tv_real_T{T}"])) < 1e-5
+    assert np.max(np.abs(prox_l1(v, 0.25) - d["l1_025"])) < 1e-6
+    # guard: same planes rejected as in the reference
+    out = prox_fl(d["guard_v"], 0.05, 0.34, 1)
+    assert np.max(np.abs(out - d["guard_out"])) < 1e-5
+
+
+def test_prox_spec_pins():
+    from paper_1904_04884_b200 import prox_fl, prox_l1, prox_tv_2d
+    assert np.allclose(prox_l1(np.array([[2.0, -2.0, 0.0]]), 0.5), [[1.5, -1.5, 0.0]])
+    c = np.full((3, 40, 33), 0.3)
+    assert np.allclose(prox_tv_2d(c, 0.7, 5), c, atol=1e-7)
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal((2, 50, 70)) + 1j * rng.standard_normal((2, 50, 70))
+    # tau_l1 above the max modulus -> zero plane
+    assert np.count_nonzero(prox_fl(v, 100.0, 0.3, 5)) == 0
+    # big planes, deep halos: oracle parity over many tiles, T = 5 and 20
+    for T in (5, 20):
+        vb = (rng.standard_normal((2, 300, 260)) + 1j * rng.standard_normal((2, 300, 260))) * 0.2
+        out = prox_fl(vb, 0.05, 0.1, T)
+        ref = O.fused_prox(vb, 0.05, 0.1, T)
+        assert np.max(np.abs(out - ref)) < 2e-5, T

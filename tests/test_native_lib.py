@@ -1,0 +1,51 @@
+"""CPU: the C-ABI library loads and exports every symbol include/holo_b200.h declares.
+No compute calls: there is no GPU here."""
+import ctypes
+
+import pytest
+
+from paper_1904_04884_b200 import _native as nat
+
+
+def test_header_symbols_exported():
+    lib = nat.load()
+    declared = nat.header_functions()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    # the ctypes signature table covers the header exactly
+    assert set(nat.SIGNATURES) == set(declared)
+
+
+def test_version_and_shape_support():
+    lib = nat.load()
+    assert lib.holo_version() >= 1
+    for n in (8, 64, 256, 1024, 2048, 4096):
+        assert lib.holo_shape_supported(n, n) == 1
+    assert lib.holo_shape_supported(1024, 256) == 1
+    for bad in (96, 100, 4, 8192, 0):
+        assert lib.holo_shape_supported(bad, 64) == 0
+
+
+def test_invalid_arguments_are_status_codes_not_crashes():
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    assert lib.holo_create(None, 0, ctypes.byref(h)) == nat.HOLO_ERR_INVALID
+    g = nat.Geometry(64, 64, 0, 1e-5, 1e-5, 5e-3, 632e-9)
+    assert lib.holo_create(ctypes.byref(g), 0, ctypes.byref(h)) == nat.HOLO_ERR_INVALID
+    assert "voxel counts" in nat.last_error()
+    g = nat.Geometry(96, 64, 4, 1e-5, 1e-5, 5e-3, 632e-9)
+    assert lib.holo_create(ctypes.byref(g), 0, ctypes.byref(h)) == nat.HOLO_ERR_UNSUPPORTED
+    with pytest.raises(ValueError):
+        nat.check(nat.HOLO_ERR_UNSUPPORTED)
+    assert lib.holo_destroy(None) == nat.HOLO_OK
+    assert lib.holo_solve(None, None, None, None) == nat.HOLO_ERR_INVALID
+
+
+def test_struct_layouts_match_header():
+    # field order / sizes of the C structs (holo_geometry, holo_solver_config, holo_report)
+    assert ctypes.sizeof(nat.Geometry) == 3 * 4 + 4 + 4 * 8  # int32 x3, pad, 4 doubles
+    assert nat.Geometry.pitch.offset == 16
+    assert nat.SolverConfig.step_size.offset == 32
+    assert nat.Report.step_size.offset == 24
+    assert nat.Report.nnz.offset == 56
