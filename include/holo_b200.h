@@ -14,7 +14,9 @@
  *   - device pointers are CUDA device addresses on the handle's device;
  *     complex data is interleaved float32 (re, im) = complex64, planes are
  *     row-major (ny rows of nx samples), stacks plane-major.
- *   - `stream` is a cudaStream_t passed as void* (NULL = the handle's stream).
+ *   - `stream` is a cudaStream_t passed as void*; NULL is the legacy default
+ *     stream (CUDA convention).  Host-buffer calls (holo_solve, *_host) run
+ *     on the handle's private stream and synchronise before returning.
  *   - calls are stream-ordered; only calls returning host data synchronise.
  *   - one handle per thread at a time.
  */

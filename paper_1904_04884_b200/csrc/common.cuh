@@ -21,6 +21,45 @@ HD float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 HD float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 HD float2 czero() { return make_float2(0.f, 0.f); }
 
+// Packed fp32x2 arithmetic (sm_100 FADD2/FMUL2/FFMA2): one instruction
+// updates a (re, im) pair, used where both parts follow the same formula.
+HD unsigned long long pk2(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+HD float2 upk2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+HD float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+HD float2 sub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+HD float2 mul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+// a * b + c
+HD float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(d);
+}
+HD float2 splat2(float a) { return make_float2(a, a); }
+
+// single-instruction MUFU approximations (rel. error ~2^-22), no IEEE slow paths
+HD float rsqrt_a(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+HD float sqrt_a(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // exp(2*pi*i * ph / 2^64).  ph is the transfer phase in cycles as a 64-bit
 // binary fraction, so "mod 1" is free integer wrap-around.  The top 8 bits
 // index a 256-entry unit-circle table (fp64-exact entries); the remaining

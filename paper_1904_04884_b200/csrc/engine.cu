@@ -21,6 +21,7 @@
 #include <vector>
 
 #ifdef HOLO_WITH_NCCL
+#include <dlfcn.h>
 #include <nccl.h>
 #endif
 
@@ -60,6 +61,45 @@ static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+
+#ifdef HOLO_WITH_NCCL
+// NCCL is resolved at run time (dlopen), not linked: in a process that already
+// loaded PyTorch this binds to torch's bundled libnccl.so.2, and a process
+// that never shards never loads NCCL at all.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.getErrorString;
+    }
+  }
+  return api;
+}
+#define ncclGetUniqueId(...) holo::nccl().getUniqueId(__VA_ARGS__)
+#define ncclCommInitRank(...) holo::nccl().commInitRank(__VA_ARGS__)
+#define ncclAllReduce(...) holo::nccl().allReduce(__VA_ARGS__)
+#define ncclCommDestroy(...) holo::nccl().commDestroy(__VA_ARGS__)
+#define ncclGetErrorString(...) holo::nccl().getErrorString(__VA_ARGS__)
+#endif
 
 template <class T>
 static cudaError_t dalloc(T*& p, size_t count) {
@@ -191,7 +231,8 @@ struct Engine {
     stream = nullptr;
   }
 
-  cudaStream_t st(void* s) const { return s ? (cudaStream_t)s : stream; }
+  // caller-supplied stream, CUDA convention: NULL is the legacy default stream
+  static cudaStream_t st(void* s) { return (cudaStream_t)s; }
 
   int init(const holo_geometry& g, int dev, int r, int n) {
     geom = g;
@@ -269,6 +310,7 @@ struct Engine {
       bt[i] = (float)((t - 1.0) / tn);
       t = tn;
     }
+    for (int i = 0; i < inner && i < 16; ++i) a.fgpb[i] = bt[i];
     HOLO_CUDA(cudaMemcpyAsync(fgp_beta, bt.data(), sizeof(float) * inner, cudaMemcpyHostToDevice, s));
     HOLO_CUDA(cudaStreamSynchronize(s));  // bt is a stack buffer
     a.fgp_beta = fgp_beta;
@@ -588,6 +630,7 @@ int holo_create(const holo_geometry* geom, int device, holo_handle** out) {
 int holo_nccl_unique_id(void* out128) {
 #ifdef HOLO_WITH_NCCL
   if (!out128) return fail(HOLO_ERR_INVALID, "null argument");
+  if (!holo::nccl().ok) return fail(HOLO_ERR_NCCL, "libnccl.so.2 not loadable");
   ncclUniqueId id;
   ncclResult_t r = ncclGetUniqueId(&id);
   if (r != ncclSuccess) return fail(HOLO_ERR_NCCL, ncclGetErrorString(r));
@@ -605,6 +648,7 @@ int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_
   if (nranks == 1) return holo_create(geom, device, out);
 #ifdef HOLO_WITH_NCCL
   if (!nccl_unique_id) return fail(HOLO_ERR_INVALID, "null nccl id");
+  if (!holo::nccl().ok) return fail(HOLO_ERR_NCCL, "libnccl.so.2 not loadable");
   TRY({
     auto* h = new holo_handle();
     int rc = h->e.init(*geom, device, rank, nranks);

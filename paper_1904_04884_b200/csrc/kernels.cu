@@ -17,6 +17,7 @@
 //   sparsevol.py:75-88 (from_dense)              -> K7
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -835,6 +836,12 @@ cudaError_t final_sum(const double* part, int n, double scale, double* out, cuda
 }
 
 size_t prox_setup(ProxArgs& a, int ny, int nx, int inner) {
+  if (prox_strip_applicable(ny, nx, inner) && !getenv("HOLO_PROX_GENERIC")) {
+    prox_strip_setup(a, ny, nx, inner);
+    a.kind = 1;
+    return 0;
+  }
+  a.kind = 0;
   a.ny = ny;
   a.nx = nx;
   a.P = (long long)ny * nx;
@@ -854,11 +861,16 @@ size_t prox_setup(ProxArgs& a, int ny, int nx, int inner) {
 bool prox_supported(int ny, int nx, int inner) {
   ProxArgs a;
   prox_setup(a, ny, nx, inner);
+  if (a.kind == 1) return true;
   const int ew = std::min(nx, a.tile + 2 * a.halo), eh = std::min(ny, a.tile + 2 * a.halo);
   return ew * eh <= kProxThreads * kProxMaxPx;
 }
 
 cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
+  if (a.kind == 1) {
+    COUNT_LAUNCH(1);
+    return prox_strip(a, s);
+  }
   const int ew = std::min(a.nx, a.tile + 2 * a.halo), eh = std::min(a.ny, a.tile + 2 * a.halo);
   if (ew * eh > kProxThreads * kProxMaxPx) return cudaErrorInvalidValue;
   const size_t smem = sizeof(float) * 6 * (size_t)ew * eh;

@@ -33,7 +33,9 @@ struct ProxArgs {
   float beta = 0.f, step = 0.f;  // y = (1+beta) x - beta xp ; v = y - step * grad
   float tau_l1 = 0.f, tau_tv = 0.f, lr_tv = 0.f;
   int inner = 0, halo = 0, tile = 0, tiles_x = 0, tiles_per_plane = 0;
-  const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule
+  int kind = 0;  // 0: generic tile kernel, 1: 64x64 register-strip kernel
+  const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule (device)
+  float fgpb[16] = {};              // same schedule by value (strip kernel, inner <= 12)
   const uint8_t* force = nullptr;   // guard fix-up pass: per plane bit0 re / bit1 im -> identity
   double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts]
 };
@@ -67,6 +69,11 @@ cudaError_t final_sum(const double* part, int n, double scale, double* out, cuda
 // prox: tile geometry chosen by prox_setup (fills halo/tile/tiles_*); returns smem bytes
 size_t prox_setup(ProxArgs& a, int ny, int nx, int inner);
 bool prox_supported(int ny, int nx, int inner);
+// register-strip prox (prox_strip.cu): used when the halo T+2 <= prox_strip_max_halo()
+int prox_strip_max_halo();
+bool prox_strip_applicable(int ny, int nx, int inner);
+void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner);
+cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s);
 cudaError_t prox(const ProxArgs& a, cudaStream_t s);
 // per-plane reduction of the prox partials + guard check.  force_acc[plane]
 // accumulates the guard bits; plane_out[plane*4 + {0..3}] = ip, dx2, l1, tv;
