@@ -163,7 +163,7 @@ def _cpu_sample(args):
     return nx * ny * nzs * res.iterations, dt
 
 
-def cpu_sample_spec(cfg, planes=8, iters=1):
+def cpu_sample_spec(cfg, planes=16, iters=1):
     nx, ny, nz, _, _, _, l1, tv, inner, _ = cfg
     return planes, iters, f"{nx}x{ny}x{planes} planes x {iters} FISTA iteration (step 1/(2*{planes})), " \
                           f"same hologram, lambda=({l1},{tv}), T={inner}; per-voxel cost is nz-independent"
