@@ -1,4 +1,4 @@
-// K4 (v3): fused-lasso prox on 64x64 register-strip regions (planes >= 64x64).
+// K4 (v4): fused-lasso prox on 64x64 register-strip regions (planes >= 64x64).
 //
 // Semantics are those of prox.py:104-148 (FGP-TV on Re and Im, step 1/(8 tau),
 // replicated edges, per-plane guard) followed by prox.py:83-96 (complex soft
@@ -13,31 +13,34 @@
 // no down/right D^T term) or at least H pixels from every interior pixel
 // (garbage that cannot reach the interior in T+2 steps).  No per-pixel masks.
 //
-// 512 threads = 16 warps: warp w covers columns 32*(w&1)..+32 (lane = column)
-// and rows 8*(w>>1)..+8; each thread keeps its 8-pixel vertical strip in
-// registers as packed (re, im) float2, so vertical neighbours are free,
-// horizontal neighbours are warp shuffles, and only the warp seam (columns
-// 31|32) and the strip ends go through ~10 KB of shared memory.  The (re, im)
-// pairs run the same formula, so the arithmetic is FADD2/FMUL2/FFMA2.
+// 512 threads = 16 warps; warp w owns rows 4w..4w+3 of all 64 columns and
+// lane l owns columns 2l, 2l+1, so each thread keeps a 4x2 tile of packed
+// (re, im) float2 state in registers: the in-tile neighbours are register
+// reads, the column neighbour across lanes is one warp shuffle per row, and
+// only the band ends (row 4w-1 / 4w+4) go through ~24 KB of shared memory.
+// Loads/stores are 16-byte (two complex64) per lane, 512 B per warp per row.
+// The FGP A/B half-steps are fused into one sweep down the band per
+// iteration, and the (re, im) arithmetic is packed FADD2/FMUL2/FFMA2.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace holo {
 namespace {
 
-constexpr int RW = 64;  // region width: 2 warps of 32 columns
-constexpr int SR = 8;   // rows per thread strip
-constexpr int NS = 8;   // strips (warp rows)
-constexpr int RH = SR * NS;
-constexpr int NT = 2 * 32 * NS;
+constexpr int RW = 64;  // region width: one warp, 2 columns per lane
+constexpr int SR = 4;   // rows per thread
+constexpr int NW = 16;  // warps = row bands
+constexpr int RH = SR * NW;
+constexpr int NT = 32 * NW;
 
-struct Seams {
-  float2 colR[2][2][RH];  // [buf][wx]: wx=0: column 32 values (right neighbour of column 31); wx=1: zeros
-  float2 colL[RH];        // column 31 values -> left neighbour of column 32
-  float2 top[2][NS][RW];  // [buf] strip top-row values -> down neighbour of the strip above
-  float2 bot[NS][RW];     // strip bottom-row values -> up neighbour of the strip below
+struct Bands {
+  float4 top[2][NW][RW / 2];  // [buf][band][lane]: row-0 values (2 columns) -> down neighbour of the band above
+  float4 bot[NW][RW / 2];     // row-(SR-1) values -> up neighbour of the band below
 };
 
+HD float4 f4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+HD float2 lo2(float4 a) { return make_float2(a.x, a.y); }
+HD float2 hi2(float4 a) { return make_float2(a.z, a.w); }
 HD float2 shfl_dn(float2 x) {
   return make_float2(__shfl_down_sync(0xffffffffu, x.x, 1), __shfl_down_sync(0xffffffffu, x.y, 1));
 }
@@ -49,7 +52,7 @@ HD float2 norm_pair(float2 a, float2 b) {
   const float2 n2 = fma2(a, a, mul2(b, b));
   return make_float2(sqrt_a(n2.x), sqrt_a(n2.y));
 }
-// projection of the dual pair onto the unit ball, per part: (pn, qn) /= max(1, |(pn, qn)|)
+// (pn, qn) /= max(1, |(pn, qn)|) for each of the (re, im) parts
 HD void project(float2& pn, float2& qn) {
   const float2 n2 = fma2(pn, pn, mul2(qn, qn));
   const float rx = rsqrt_a(n2.x), ry = rsqrt_a(n2.y);  // unconditional MUFU, then select
@@ -66,222 +69,270 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
     force = a.force[plane];
     if (!force) return;  // fix-up pass: only planes whose guard fired
   }
-  __shared__ Seams sm;
+  __shared__ Bands sm;
   const int TI = a.tile, H = a.halo;
   const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
   const int i0 = ty * TI, j0 = tx * TI;
   const int i1 = min(a.ny, i0 + TI), j1 = min(a.nx, j0 + TI);
   const int ri0 = min(max(i0 - H, 0), a.ny - RH);  // region clamped into the plane
   const int rj0 = min(max(j0 - H, 0), a.nx - RW);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wx = w & 1, wy = w >> 1;
-  const int c = wx * 32 + lane, r0 = wy * SR;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool lane0 = lane == 0, lane31 = lane == 31;
-  const bool seam_w = (wx == 0) && lane31;  // writes column 31 (left-neighbour seam)
-  const bool seam_e = (wx == 1) && lane0;   // writes column 32 (right-neighbour seam)
-  const bool self_left = lane0 && wx == 0;  // region's left column: zero x-difference
-  const int gj = rj0 + c;
-  const bool colInt = gj >= j0 && gj < j1;
+  const int r0 = w * SR;
+  const int gj = rj0 + 2 * lane;  // columns gj, gj+1
+  // interior bits: bit (2 s + k) for row s, column k
   uint32_t mInt = 0;
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
     const int gi = ri0 + r0 + s;
-    if (colInt && gi >= i0 && gi < i1) mInt |= 1u << s;
-  }
-  if (threadIdx.x < RH) {
-    sm.colR[0][1][threadIdx.x] = make_float2(0.f, 0.f);
-    sm.colR[1][1][threadIdx.x] = make_float2(0.f, 0.f);
+    const bool rowInt = gi >= i0 && gi < i1;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (rowInt && gj + k >= j0 && gj + k < j1) mInt |= 1u << (2 * s + k);
   }
   const long long g0 = (long long)plane * a.P + (long long)(ri0 + r0) * a.nx + gj;
 
-  float2 v[SR], p[SR], q[SR], rp[SR], rq[SR];
+  float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
   {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
       const long long g = g0 + (long long)s * a.nx;
-      float2 y = a.x[g];
-      if (a.beta != 0.f) y = fma2(cb, y, mul2(cm, a.xp[g]));
-      if (a.grad) y = fma2(cs, a.grad[g], y);
-      v[s] = y;
+      float4 y = *reinterpret_cast<const float4*>(a.x + g);
+      float2 y0 = lo2(y), y1 = hi2(y);
+      if (a.beta != 0.f) {
+        const float4 o = *reinterpret_cast<const float4*>(a.xp + g);
+        y0 = fma2(cb, y0, mul2(cm, lo2(o)));
+        y1 = fma2(cb, y1, mul2(cm, hi2(o)));
+      }
+      if (a.grad) {
+        const float4 gg = *reinterpret_cast<const float4*>(a.grad + g);
+        y0 = fma2(cs, lo2(gg), y0);
+        y1 = fma2(cs, hi2(gg), y1);
+      }
+      v[s][0] = y0;
+      v[s][1] = y1;
     }
   }
 
-  // per-thread partial sums over its <= 8 pixels (fp32), promoted to fp64 at the end
+  // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
   float acc[kProxParts];
 #pragma unroll
   for (int i = 0; i < kProxParts; ++i) acc[i] = 0.f;
 
-  // values other threads read as "up" (strip bottom row) and "left" (seam column 31)
-  auto publish_ul = [&](const float2 (&x)[SR]) {
-    sm.bot[wy][c] = x[SR - 1];
-    if (seam_w) {
-#pragma unroll
-      for (int s = 0; s < SR; ++s) sm.colL[r0 + s] = x[s];
-    }
+  // x-differences and TV contributions of one row (both columns): left neighbour
+  // of column 0 is lane-1's column 1 (own value at the region's left edge)
+  auto gx_row = [&](float2 x0, float2 x1, float2& gx0, float2& gx1) {
+    const float2 l = shfl_up(x1);
+    gx0 = lane0 ? make_float2(0.f, 0.f) : sub2(x0, l);
+    gx1 = sub2(x1, x0);
   };
-  // values other threads read as "down" (strip top row) and "right" (seam column 32)
-  auto publish_dr = [&](int b, const float2 (&dn)[SR], const float2 (&rt)[SR]) {
-    sm.top[b][wy][c] = dn[0];
-    if (seam_e) {
-#pragma unroll
-      for (int s = 0; s < SR; ++s) sm.colR[b][0][r0 + s] = rt[s];
-    }
+  // right neighbour of column 1 = lane+1's column 0 (0 beyond the region)
+  auto right_of = [&](float2 x0) {
+    const float2 r = shfl_dn(x0);
+    return lane31 ? make_float2(0.f, 0.f) : r;
   };
-  // left neighbour of row s (own value at the region's left edge: zero difference)
-  auto left_of = [&](float2 x, int s) {
-    const float2 l = shfl_up(x);
-    if (lane0) return self_left ? x : sm.colL[r0 + s];
-    return l;
+  auto above_of = [&](int k, float2 self) -> float2 {
+    if (w == 0) return self;  // region top row: zero y-difference
+    const float4 b4 = sm.bot[w - 1][lane];
+    return k ? hi2(b4) : lo2(b4);
   };
   const float2 mtau = splat2(-a.tau_tv);
 
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
-    publish_ul(v);
+    sm.bot[w][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     __syncthreads();
     {
-      float2 up = (wy > 0) ? sm.bot[wy - 1][c] : v[0];
+      float2 up0 = above_of(0, v[0][0]), up1 = above_of(1, v[0][1]);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
-        const float2 gy = sub2(v[s], up);
-        const float2 gx = sub2(v[s], left_of(v[s], s));
-        up = v[s];
-        if (mInt & (1u << s)) {
-          const float2 nv = norm_pair(gy, gx);
+        float2 gx0, gx1;
+        gx_row(v[s][0], v[s][1], gx0, gx1);
+        const float2 gy0 = sub2(v[s][0], up0), gy1 = sub2(v[s][1], up1);
+        up0 = v[s][0];
+        up1 = v[s][1];
+        if (mInt & (1u << (2 * s))) {
+          const float2 nv = norm_pair(gy0, gx0);
           acc[PT_TVV_R] += nv.x;
           acc[PT_TVV_I] += nv.y;
         }
-        float2 pn = mul2(lr2, gy), qn = mul2(lr2, gx);
-        project(pn, qn);
-        p[s] = rp[s] = pn;
-        q[s] = rq[s] = qn;
+        if (mInt & (2u << (2 * s))) {
+          const float2 nv = norm_pair(gy1, gx1);
+          acc[PT_TVV_R] += nv.x;
+          acc[PT_TVV_I] += nv.y;
+        }
+        float2 pn0 = mul2(lr2, gy0), qn0 = mul2(lr2, gx0);
+        float2 pn1 = mul2(lr2, gy1), qn1 = mul2(lr2, gx1);
+        project(pn0, qn0);
+        project(pn1, qn1);
+        p[s][0] = rp[s][0] = pn0;
+        q[s][0] = rq[s][0] = qn0;
+        p[s][1] = rp[s][1] = pn1;
+        q[s][1] = rq[s][1] = qn1;
       }
     }
-    publish_dr(0, rp, rq);
+    sm.top[0][w][lane] = f4(rp[0][0], rp[0][1]);
     __syncthreads();
-    // ---- iterations 1..T-1: one fused sweep down the strip per iteration ----
+    // ---- iterations 1..T-1: one fused sweep down the band per iteration ----
     for (int t = 1; t < a.inner; ++t) {
-      const int b = (t - 1) & 1;  // buffer holding this iteration's rp-top / rq-seam
+      const int b = (t - 1) & 1;  // buffer holding this iteration's band-top rp
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
-      // u of row s = v - tau (rp[s] + rq[s] - rp[s+1] - rq_right[s])
-      auto urow = [&](int s, float2 rp_next, float2 rq_right) {
-        return fma2(mtau, sub2(sub2(add2(rp[s], rq[s]), rp_next), rq_right), v[s]);
+      // u(s, k) = v - tau (rp + rq - rp_down - rq_right)
+      auto urow = [&](int s, float2 rpd0, float2 rpd1, float2& u0, float2& u1) {
+        const float2 rqr1 = right_of(rq[s][0]);
+        u0 = fma2(mtau, sub2(sub2(add2(rp[s][0], rq[s][0]), rpd0), rq[s][1]), v[s][0]);
+        u1 = fma2(mtau, sub2(sub2(add2(rp[s][1], rq[s][1]), rpd1), rqr1), v[s][1]);
       };
-      // pre-pass: the rows other threads need before the sweep (strip bottom, seam column)
-      const float2 rp_below = (wy < NS - 1) ? sm.top[b][wy + 1][c] : make_float2(0.f, 0.f);
-      float2 rq_r7 = shfl_dn(rq[SR - 1]);
-      if (lane31) rq_r7 = sm.colR[b][wx][r0 + SR - 1];
-      const float2 u7 = urow(SR - 1, rp_below, rq_r7);
-      sm.bot[wy][c] = u7;
-      if (seam_w) {
-#pragma unroll
-        for (int s = 0; s < SR - 1; ++s) sm.colL[r0 + s] = urow(s, rp[s + 1], sm.colR[b][0][r0 + s]);
-        sm.colL[r0 + SR - 1] = u7;
+      // pre-pass: the band's last row, needed by the band below before its sweep
+      float2 ul0, ul1;
+      {
+        const float4 d4 = (w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        urow(SR - 1, lo2(d4), hi2(d4), ul0, ul1);
       }
+      sm.bot[w][lane] = f4(ul0, ul1);
       __syncthreads();
-      float2 up = (wy > 0) ? sm.bot[wy - 1][c] : make_float2(0.f, 0.f);
+      float2 up0 = above_of(0, make_float2(0.f, 0.f)), up1 = above_of(1, make_float2(0.f, 0.f));
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
-        float2 u;
+        float2 u0, u1;
         if (s == SR - 1) {
-          u = u7;
+          u0 = ul0;
+          u1 = ul1;
         } else {
-          float2 rq_r = shfl_dn(rq[s]);
-          if (lane31) rq_r = sm.colR[b][wx][r0 + s];
-          u = urow(s, rp[s + 1], rq_r);
+          urow(s, rp[s + 1][0], rp[s + 1][1], u0, u1);
         }
-        if (s == 0 && wy == 0) up = u;  // region top row: zero y-difference
-        const float2 gy = sub2(u, up);
-        const float2 gx = sub2(u, left_of(u, s));
-        up = u;
-        float2 pn = fma2(lr2, gy, rp[s]);
-        float2 qn = fma2(lr2, gx, rq[s]);
-        project(pn, qn);
-        rp[s] = fma2(bt2, sub2(pn, p[s]), pn);
-        rq[s] = fma2(bt2, sub2(qn, q[s]), qn);
-        p[s] = pn;
-        q[s] = qn;
+        if (s == 0 && w == 0) {  // region top row: zero y-difference
+          up0 = u0;
+          up1 = u1;
+        }
+        float2 gx0, gx1;
+        gx_row(u0, u1, gx0, gx1);
+        const float2 gy0 = sub2(u0, up0), gy1 = sub2(u1, up1);
+        up0 = u0;
+        up1 = u1;
+        float2 pn0 = fma2(lr2, gy0, rp[s][0]), qn0 = fma2(lr2, gx0, rq[s][0]);
+        float2 pn1 = fma2(lr2, gy1, rp[s][1]), qn1 = fma2(lr2, gx1, rq[s][1]);
+        project(pn0, qn0);
+        project(pn1, qn1);
+        rp[s][0] = fma2(bt2, sub2(pn0, p[s][0]), pn0);
+        rq[s][0] = fma2(bt2, sub2(qn0, q[s][0]), qn0);
+        rp[s][1] = fma2(bt2, sub2(pn1, p[s][1]), pn1);
+        rq[s][1] = fma2(bt2, sub2(qn1, q[s][1]), qn1);
+        p[s][0] = pn0;
+        q[s][0] = qn0;
+        p[s][1] = pn1;
+        q[s][1] = qn1;
       }
-      publish_dr(b ^ 1, rp, rq);  // other buffer: slower warps may still read buffer b
+      sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffer: slower warps may read b
       __syncthreads();
     }
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
-    const int bf = (a.inner - 1) & 1;  // the buffer not read by the last sweep
-    publish_dr(bf ^ 1, p, q);
+    const int bf = a.inner & 1;  // not read by the last sweep
+    sm.top[bf][w][lane] = f4(p[0][0], p[0][1]);
     __syncthreads();
     {
-      const float2 p_below = (wy < NS - 1) ? sm.top[bf ^ 1][wy + 1][c] : make_float2(0.f, 0.f);
+      const float4 d4 = (w < NW - 1) ? sm.top[bf][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
-        float2 q_r = shfl_dn(q[s]);
-        if (lane31) q_r = sm.colR[bf ^ 1][wx][r0 + s];
-        const float2 pd = (s < SR - 1) ? p[s + 1] : p_below;
-        rp[s] = fma2(mtau, sub2(sub2(add2(p[s], q[s]), pd), q_r), v[s]);
+        const float2 pd0 = (s < SR - 1) ? p[s + 1][0] : lo2(d4);
+        const float2 pd1 = (s < SR - 1) ? p[s + 1][1] : hi2(d4);
+        const float2 qr1 = right_of(q[s][0]);
+        rp[s][0] = fma2(mtau, sub2(sub2(add2(p[s][0], q[s][0]), pd0), q[s][1]), v[s][0]);
+        rp[s][1] = fma2(mtau, sub2(sub2(add2(p[s][1], q[s][1]), pd1), qr1), v[s][1]);
       }
     }
-    publish_ul(rp);  // bot/colL last read by the final sweep, a sync ago
+    sm.bot[w][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
-      float2 up = (wy > 0) ? sm.bot[wy - 1][c] : rp[0];
+      float2 up0 = above_of(0, rp[0][0]), up1 = above_of(1, rp[0][1]);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
-        const float2 gy = sub2(rp[s], up);
-        const float2 gx = sub2(rp[s], left_of(rp[s], s));
-        up = rp[s];
-        if (mInt & (1u << s)) {
-          const float2 nw = norm_pair(gy, gx);
-          const float2 dv = sub2(rp[s], v[s]);
-          acc[PT_TVW_R] += nw.x;
-          acc[PT_TVW_I] += nw.y;
-          acc[PT_D2_R] += dv.x * dv.x;
-          acc[PT_D2_I] += dv.y * dv.y;
+        float2 gx0, gx1;
+        gx_row(rp[s][0], rp[s][1], gx0, gx1);
+        const float2 gy0 = sub2(rp[s][0], up0), gy1 = sub2(rp[s][1], up1);
+        up0 = rp[s][0];
+        up1 = rp[s][1];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (mInt & (1u << (2 * s + k))) {
+            const float2 nw = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
+            const float2 dv = sub2(rp[s][k], v[s][k]);
+            acc[PT_TVW_R] += nw.x;
+            acc[PT_TVW_I] += nw.y;
+            acc[PT_D2_R] += dv.x * dv.x;
+            acc[PT_D2_I] += dv.y * dv.y;
+          }
         }
       }
     }
-    __syncthreads();  // bot/colL reads done before x_new is published
+    __syncthreads();  // bot reads done before x_new is published
   } else {
 #pragma unroll
-    for (int s = 0; s < SR; ++s) rp[s] = v[s];
+    for (int s = 0; s < SR; ++s) {
+      rp[s][0] = v[s][0];
+      rp[s][1] = v[s][1];
+    }
   }
 
   // soft threshold of w (fix-up pass: identity part where the guard fired); x_new -> p
   const float tl = a.tau_l1;
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
-    const float wr = (force & 1u) ? v[s].x : rp[s].x;
-    const float wi = (force & 2u) ? v[s].y : rp[s].y;
-    const float n2 = fmaf(wr, wr, wi * wi);
-    const float shrink = 1.f - tl * rsqrt_a(n2);
-    const float gsc = (tl > 0.f) ? ((n2 > tl * tl) ? shrink : 0.f) : 1.f;
-    p[s] = make_float2(wr * gsc, wi * gsc);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float wr = (force & 1u) ? v[s][k].x : rp[s][k].x;
+      const float wi = (force & 2u) ? v[s][k].y : rp[s][k].y;
+      const float n2 = fmaf(wr, wr, wi * wi);
+      const float shrink = 1.f - tl * rsqrt_a(n2);
+      const float gsc = (tl > 0.f) ? ((n2 > tl * tl) ? shrink : 0.f) : 1.f;
+      p[s][k] = make_float2(wr * gsc, wi * gsc);
+    }
   }
-  publish_ul(p);
+  sm.bot[w][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
   __syncthreads();
   {
-    float2 up = (wy > 0) ? sm.bot[wy - 1][c] : p[0];
+    float2 up0 = above_of(0, p[0][0]), up1 = above_of(1, p[0][1]);
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta);
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
-      const float2 gy = sub2(p[s], up);
-      const float2 gx = sub2(p[s], left_of(p[s], s));
-      up = p[s];
-      if (!(mInt & (1u << s))) continue;
-      const float2 nx2 = norm_pair(gy, gx);
-      acc[PT_TVX_R] += nx2.x;
-      acc[PT_TVX_I] += nx2.y;
-      acc[PT_L1] += sqrt_a(fmaf(p[s].x, p[s].x, p[s].y * p[s].y));
+      float2 gx0, gx1;
+      gx_row(p[s][0], p[s][1], gx0, gx1);
+      const float2 gy0 = sub2(p[s][0], up0), gy1 = sub2(p[s][1], up1);
+      up0 = p[s][0];
+      up1 = p[s][1];
+      const uint32_t rowbits = (mInt >> (2 * s)) & 3u;
+      if (!rowbits) continue;
       const long long g = g0 + (long long)s * a.nx;
-      float2 y = a.x[g];
-      if (a.beta != 0.f) y = fma2(cb, y, mul2(cm, a.xp[g]));
-      const float2 dx = sub2(p[s], y);
-      if (a.grad) {
-        const float2 gg = a.grad[g];
-        acc[PT_IP] += fmaf(gg.x, dx.x, gg.y * dx.y);
+      float4 y4 = *reinterpret_cast<const float4*>(a.x + g);
+      float2 y[2] = {lo2(y4), hi2(y4)};
+      if (a.beta != 0.f) {
+        const float4 o = *reinterpret_cast<const float4*>(a.xp + g);
+        y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
+        y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
       }
-      acc[PT_DX2] += fmaf(dx.x, dx.x, dx.y * dx.y);
-      a.xnew[g] = p[s];
+      float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.grad) gr4 = *reinterpret_cast<const float4*>(a.grad + g);
+      const float2 gr[2] = {lo2(gr4), hi2(gr4)};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!(rowbits & (1u << k))) continue;
+        const float2 nx2 = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
+        acc[PT_TVX_R] += nx2.x;
+        acc[PT_TVX_I] += nx2.y;
+        acc[PT_L1] += sqrt_a(fmaf(p[s][k].x, p[s][k].x, p[s][k].y * p[s][k].y));
+        const float2 dx = sub2(p[s][k], y[k]);
+        acc[PT_IP] += fmaf(gr[k].x, dx.x, gr[k].y * dx.y);
+        acc[PT_DX2] += fmaf(dx.x, dx.x, dx.y * dx.y);
+      }
+      if (rowbits == 3u) {
+        *reinterpret_cast<float4*>(a.xnew + g) = f4(p[s][0], p[s][1]);
+      } else {
+        if (rowbits & 1u) a.xnew[g] = p[s][0];
+        if (rowbits & 2u) a.xnew[g + 1] = p[s][1];
+      }
     }
   }
   double accd[kProxParts];
@@ -295,16 +346,24 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
 int prox_strip_max_halo() { return 14; }
 
 bool prox_strip_applicable(int ny, int nx, int inner) {
-  return ny >= RH && nx >= RW && inner + 2 <= prox_strip_max_halo() && inner <= 16;
+  return ny >= RH && nx >= RW && (nx % 2) == 0 && inner <= 12;
 }
 
+// Halo widths.  Garbage from a region edge that is not a plane edge advances
+// one pixel per dependent step: from the top/left edge T B-steps (which read
+// the up/left neighbour) plus the TV of w / x_new (also up/left) -> T+1; from
+// the bottom/right edge T-1 A-steps plus the final D^T (down/right) -> T.
+// The leading halo is rounded up to even (16-byte aligned float4 lanes) and
+// the trailing one so the tile is even.
 void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.ny = ny;
   a.nx = nx;
   a.P = (long long)ny * nx;
   a.inner = inner;
-  a.halo = inner + 2;
-  a.tile = RW - 2 * a.halo;
+  const int h_lo = (inner + 2) & ~1;          // >= T+1, even
+  const int h_hi = inner + (inner & 1);       // >= T, tile even
+  a.halo = h_lo;
+  a.tile = RW - h_lo - h_hi;
   a.tiles_x = (nx + a.tile - 1) / a.tile;
   a.tiles_per_plane = a.tiles_x * ((ny + a.tile - 1) / a.tile);
 }
