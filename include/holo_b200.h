@@ -56,6 +56,7 @@ typedef struct {
   double step_size;
   double bt_shrink, stop_tol;
   int32_t log_objective;
+  int32_t real_nonnegative; /* solver.py:154-216 _RealEngine: x real, x >= 0; needs step_size > 0 */
 } holo_solver_config;
 
 /* solver.py:71-85 SolveReport (+ counters the reference keeps internally). */
@@ -83,12 +84,15 @@ int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_
 int holo_destroy(holo_handle* h);
 int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end);
 
-/* solver.py:225-247 estimate_operator_norm (complex engine): ||A||^2.  The
- * complex engine has A A^H = nz * (band projector), so the power iteration
- * converges to nz in one step; this returns that closed form.  The GPU
- * power iteration itself is holo_power_iteration. */
-int holo_operator_norm(holo_handle* h, double* sigma2);
-int holo_power_iteration(holo_handle* h, int iters, uint64_t seed, double* sigma2);
+/* Exact ||A||^2.  Complex engine: A A^H = nz * (band projector), so nz (the
+ * value solver.py:225-247's power iteration converges to after one step).
+ * Real engine (real != 0): max over the band of sum_k cos^2(phase_k). */
+int holo_operator_norm(holo_handle* h, int32_t real, double* sigma2);
+/* solver.py:225-247 estimate_operator_norm: `iters` power-iteration steps of
+ * A^H A from the caller's start vector v0 (device, complex64, local planes,
+ * unit norm; real != 0 uses Re(v0) and the real engine).  Returns the last
+ * ||A^H A v||, exactly the reference's estimate for the same v0. */
+int holo_power_iteration(holo_handle* h, const void* v0, int32_t iters, int32_t real, double* sigma2, void* stream);
 
 /* solver.py:254-379 fista (complex engine).  b: ny*nx real hologram residual
  * (only Re(b) is used by the reference, solver.py:274).  _host reads a host

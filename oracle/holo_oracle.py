@@ -112,6 +112,44 @@ def back_project(r: np.ndarray, g: Geometry, chunk: int = 16) -> np.ndarray:
     return out
 
 
+def cosine_stack(g: Geometry) -> np.ndarray:
+    """C_k = cos(2 pi (z0 + k dz) q) on the rfft half grid, by the fp64 angle-addition
+    recurrence of the real engine (solver.py:165-182)."""
+    fy = freq_axis(g.ny, g.pitch)
+    fx = np.fft.rfftfreq(g.nx, d=g.pitch)
+    FY, FX = np.meshgrid(fy, fx, indexing="ij")
+    arg = 1.0 - (g.wavelength * FY) ** 2 - (g.wavelength * FX) ** 2
+    keep = arg >= 0
+    root = np.sqrt(np.where(keep, arg, 0.0))
+    c = np.cos(2 * np.pi * (g.z0 / g.wavelength) * root) * keep
+    sn = np.sin(2 * np.pi * (g.z0 / g.wavelength) * root) * keep
+    cg = np.cos(2 * np.pi * (g.dz / g.wavelength) * root)
+    sg = np.sin(2 * np.pi * (g.dz / g.wavelength) * root)
+    out = np.empty((g.nz,) + c.shape)
+    for k in range(g.nz):
+        out[k] = c
+        c, sn = c * cg - sn * sg, c * sg + sn * cg
+    return out
+
+
+def real_forward(vol, g: Geometry, cs=None) -> np.ndarray:
+    """Real-nonnegative engine forward: irfft2(sum_k rfft2(Re x_k) C_k) (solver.py:184-193)."""
+    cs = cosine_stack(g) if cs is None else cs
+    spec = np.zeros(cs.shape[1:], dtype=np.complex128)
+    for k in range(g.nz):
+        xk = np.real(vol[k])
+        if np.any(xk != 0):
+            spec += np.fft.rfft2(xk) * cs[k]
+    return np.fft.irfft2(spec, s=g.shape)
+
+
+def real_back_project(r, g: Geometry, cs=None) -> np.ndarray:
+    """Real engine adjoint: plane k = irfft2(C_k rfft2(r)) (solver.py:195-200 is 2x this)."""
+    cs = cosine_stack(g) if cs is None else cs
+    rs = np.fft.rfft2(np.asarray(r, dtype=np.float64))
+    return np.fft.irfft2(cs * rs[None], s=g.shape, axes=(-2, -1))
+
+
 # ------------------------------------------------------------------ prox ----
 
 def _grad2(x):
@@ -214,26 +252,44 @@ def fused_prox(v, tau_l1: float, tau_tv: float, iters: int = 5):
 
 # ---------------------------------------------------------------- solver ----
 
-def power_norm(g: Geometry, iters: int = 10, seed: int = 0) -> float:
-    """||A||^2 by power iteration from default_rng(seed) (solver.py:225-247, complex engine)."""
+def power_start(g: Geometry, seed: int = 0, real: bool = False) -> np.ndarray:
+    """The power iteration's start vector: default_rng(seed) normals (solver.py:231-237)."""
     rng = np.random.default_rng(seed)
     shp = (g.nz,) + g.shape
-    v = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
-    v /= np.linalg.norm(v)
+    if real:
+        v = rng.standard_normal(shp)
+    else:
+        v = rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+    return v / np.linalg.norm(v)
+
+
+def power_norm(g: Geometry, iters: int = 10, seed: int = 0, real: bool = False) -> float:
+    """||A||^2 by power iteration from default_rng(seed) (solver.py:225-247)."""
+    v = power_start(g, seed, real)
+    cs = cosine_stack(g) if real else None
     nrm = 1.0
     for _ in range(iters):
-        w = back_project(sensor_forward(v, g, chunk=g.nz), g, chunk=64)
+        if real:
+            w = real_back_project(real_forward(v, g, cs), g, cs)
+        else:
+            w = back_project(sensor_forward(v, g, chunk=g.nz), g, chunk=64)
         nrm = float(np.linalg.norm(w))
         v = w / nrm
     return nrm
 
 
-def _penalty(vol, lam_l1, lam_tv):
-    """sum over planes of lam_l1 |x|_1 + lam_tv (TV re + TV im) (solver.py:146-151, 282-283)."""
+def _penalty(vol, lam_l1, lam_tv, real=False):
+    """sum over planes of lam_l1 |x|_1 + lam_tv (TV re + TV im) (solver.py:146-151, 282-283);
+    real engine: lam_l1 sum x + lam_tv TV(x) (solver.py:212-216)."""
     total = 0.0
     for k in range(vol.shape[0]):
         p = vol[k]
         if not np.any(p != 0):
+            continue
+        if real:
+            total += lam_l1 * float(np.sum(p.real))
+            if lam_tv > 0:
+                total += lam_tv * tv_norm(p.real)
             continue
         total += lam_l1 * float(np.sum(np.abs(p)))
         if lam_tv > 0:
@@ -253,24 +309,29 @@ class OracleResult:
 
 def fista_solve(b, g: Geometry, lam_l1=0.5, lam_tv=0.2, max_iters=100, inner=5,
                 policy="backtracking", step_size=None, shrink=0.5, stop_tol=0.0,
-                chunk=16) -> OracleResult:
-    """Dense restatement of solver.fista, complex engine (solver.py:254-379)."""
+                chunk=16, real=False) -> OracleResult:
+    """Dense restatement of solver.fista (solver.py:254-379); real=True is the
+    real-nonnegative engine (solver.py:154-216)."""
     bb = np.asarray(b, dtype=np.float64).real
     if bb.shape != g.shape:
         raise ValueError("hologram / geometry shape mismatch")
     if step_size is not None:
         step = float(step_size)
     else:
-        s2 = power_norm(g)
+        s2 = power_norm(g, real=real)
         step = 1.0 / (2.0 * s2) if s2 > 0 else 1.0
+    cs = cosine_stack(g) if real else None
+
+    def fwd(vol):
+        return real_forward(vol, g, cs) if real else sensor_forward(vol, g, chunk)
 
     def data_misfit(vol):
-        r = sensor_forward(vol, g, chunk) - bb
+        r = fwd(vol) - bb
         return float(np.sum(r * r))
 
     def attempt(y, step_local):
         # one prox-gradient step from y with backtracking (solver.py:297-327)
-        res = sensor_forward(y, g, chunk) - bb
+        res = fwd(y) - bb
         f_y = float(np.sum(res * res))
         rs = np.fft.fft2(res.astype(np.complex128))
         while True:
@@ -279,12 +340,22 @@ def fista_solve(b, g: Geometry, lam_l1=0.5, lam_tv=0.2, max_iters=100, inner=5,
             dx2 = 0.0
             for k0 in range(0, g.nz, chunk):
                 k1 = min(g.nz, k0 + chunk)
-                grad = 2.0 * np.fft.ifft2(transfer_stack(g, k0, k1) * rs[None], axes=(-2, -1))
                 yk = y[k0:k1]
-                cand = fused_prox(yk - step_local * grad, step_local * lam_l1, step_local * lam_tv, inner)
-                d = cand - yk
-                ip += float(np.sum((grad.conj() * d).real))
-                dx2 += float(np.sum((d * d.conj()).real))
+                if real:
+                    grad = 2.0 * np.fft.irfft2(cs[k0:k1] * np.fft.rfft2(res)[None], s=g.shape, axes=(-2, -1))
+                    w = yk.real - step_local * grad
+                    if lam_tv > 0:
+                        w = fgp_tv(w, step_local * lam_tv, inner)
+                    cand = np.maximum(w - step_local * lam_l1, 0.0).astype(np.complex128)
+                    d = cand.real - yk.real
+                    ip += float(np.sum(grad * d))
+                    dx2 += float(np.sum(d * d))
+                else:
+                    grad = 2.0 * np.fft.ifft2(transfer_stack(g, k0, k1) * rs[None], axes=(-2, -1))
+                    cand = fused_prox(yk - step_local * grad, step_local * lam_l1, step_local * lam_tv, inner)
+                    d = cand - yk
+                    ip += float(np.sum((grad.conj() * d).real))
+                    dx2 += float(np.sum((d * d.conj()).real))
                 new[k0:k1] = cand
             f_new = data_misfit(new)
             if policy != "backtracking":
@@ -306,12 +377,12 @@ def fista_solve(b, g: Geometry, lam_l1=0.5, lam_tv=0.2, max_iters=100, inner=5,
         beta = (t - 1.0) / tn
         y = (1.0 + beta) * x - beta * x_old if beta != 0.0 else x
         new, f_new, step = attempt(y, step)
-        obj = f_new + _penalty(new, lam_l1, lam_tv)
+        obj = f_new + _penalty(new, lam_l1, lam_tv, real)
         if obj > last and it > 0:  # adaptive restart (solver.py:339-349)
             restarts += 1
             t = tn = 1.0
             new, f_new, step = attempt(x, step)
-            obj = f_new + _penalty(new, lam_l1, lam_tv)
+            obj = f_new + _penalty(new, lam_l1, lam_tv, real)
             if obj > last:
                 new, obj = x, last
         x_old, x, t = x, new, tn

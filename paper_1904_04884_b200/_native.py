@@ -36,7 +36,7 @@ class SolverConfig(ctypes.Structure):
                 ("max_iters", ctypes.c_int32), ("tv_inner_iters", ctypes.c_int32),
                 ("step_policy", ctypes.c_int32), ("step_size", ctypes.c_double),
                 ("bt_shrink", ctypes.c_double), ("stop_tol", ctypes.c_double),
-                ("log_objective", ctypes.c_int32)]
+                ("log_objective", ctypes.c_int32), ("real_nonnegative", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):
@@ -62,8 +62,8 @@ SIGNATURES = {
                                            ctypes.POINTER(_H)]),
     "holo_destroy": (ctypes.c_int, [_H]),
     "holo_local_planes": (ctypes.c_int, [_H, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
-    "holo_operator_norm": (ctypes.c_int, [_H, ctypes.POINTER(_D)]),
-    "holo_power_iteration": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(_D)]),
+    "holo_operator_norm": (ctypes.c_int, [_H, _I, ctypes.POINTER(_D)]),
+    "holo_power_iteration": (ctypes.c_int, [_H, _P, _I, _I, ctypes.POINTER(_D), _P]),
     "holo_solve": (ctypes.c_int, [_H, _P, ctypes.POINTER(SolverConfig), ctypes.POINTER(Report)]),
     "holo_solve_device": (ctypes.c_int, [_H, _P, ctypes.POINTER(SolverConfig), ctypes.POINTER(Report), _P]),
     "holo_history": (ctypes.c_int, [_H, _P, _I, ctypes.POINTER(_I)]),

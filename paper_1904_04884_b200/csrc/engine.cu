@@ -168,7 +168,7 @@ struct Prof {
   } while (0)
 
 // host scalar block (pinned) layout
-enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_N };
+enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_AUX, SC_N };
 
 struct Engine {
   holo_geometry geom{};
@@ -206,6 +206,7 @@ struct Engine {
   long long* coo_offsets = nullptr;
   std::vector<int> h_counts;
   std::vector<long long> h_offsets;
+  double real_sigma2 = -1.0;  // cached ||A_real||^2
   // results of the last solve
   int ix = 0;  // slot holding the solution
   bool have_solution = false;
@@ -386,6 +387,51 @@ struct Engine {
     return allreduce_scalars(scal, SC_FAIL + 1, s);
   }
 
+  int real_opnorm_value(double& out, cudaStream_t s) {
+    if (real_sigma2 < 0) {
+      HOLO_CUDA(real_opnorm(plan, geom.nz, scal + SC_AUX, s));
+      if (int rc = read_scalars(s)) return rc;
+      real_sigma2 = h_scal[SC_AUX];
+    }
+    out = real_sigma2;
+    return HOLO_OK;
+  }
+
+  // solver.py:225-247: power iteration of A^H A from v0 (unit norm)
+  int power_iteration(const float2* v0, int iters, bool real, double& out, cudaStream_t s) {
+    int rc = ensure_volume();
+    if (rc) return rc;
+    const long long n = (long long)nzl * P;
+    if (n) HOLO_CUDA(cudaMemcpyAsync(X[0], v0, sizeof(float2) * n, cudaMemcpyDeviceToDevice, s));
+    float2* v = X[0];
+    if (real) HOLO_CUDA(vol_rescale(v, n, nullptr, 1, s));
+    const int nb = vol_norm2_blocks(std::max(n, 1LL));
+    double* part = nullptr;
+    HOLO_CUDA(cudaMallocAsync(&part, sizeof(double) * nb, s));
+    double nrm = 1.0;
+    for (int it = 0; it < iters; ++it) {
+      if ((rc = forward_spectrum(v, S[0], s))) return rc;  // v may be scratch: consumed in place
+      // spectrum of the real sensor field h = A v: m (S(f) + conj S(-f)) / 2
+      HOLO_CUDA(sensor(plan, S[0], nullptr, 1.f, 0.f, nullptr, R, sens_part, s));
+      if ((rc = adjoint_grad(R, 1.0f, s))) return rc;  // scratch = A^H h
+      if (real) HOLO_CUDA(vol_rescale(scratch, n, nullptr, 1, s));
+      HOLO_CUDA(cudaMemsetAsync(scal, 0, sizeof(double), s));
+      if (n) {
+        HOLO_CUDA(vol_norm2(scratch, n, part, s));
+        HOLO_CUDA(final_sum(part, nb, 1.0, scal, s));
+      }
+      if ((rc = allreduce_scalars(scal, 1, s))) return rc;
+      if ((rc = read_scalars(s))) return rc;
+      nrm = std::sqrt(h_scal[0]);
+      HOLO_CUDA(vol_rescale(scratch, n, scal, real ? 1 : 0, s));
+      v = scratch;
+    }
+    cudaFreeAsync(part, s);
+    HOLO_CUDA(cudaStreamSynchronize(s));
+    out = nrm;
+    return HOLO_OK;
+  }
+
   // solver.py:297-327 iterate_from(y, step) with y = (1+beta) x - beta xp
   int iterate_from(int sx, int sxp, double beta, double step, const holo_solver_config& cfg, Attempt& out,
                    cudaStream_t s) {
@@ -398,7 +444,8 @@ struct Engine {
     HOLO_CUDA(prof.end(s));
     int c = 0;
     while (c == sx || c == sxp) ++c;
-    const double sigma2 = (double)geom.nz;  // ||A||^2, closed form (see holo_operator_norm)
+    double sigma2 = (double)geom.nz;  // ||A||^2, closed form (see holo_operator_norm)
+    if (cfg.real_nonnegative && (rc = real_opnorm_value(sigma2, s))) return rc;
     for (;;) {
       // gradient 2 A^H r_y into scratch (the forward pass below reuses scratch,
       // so a backtracking retry recomputes it)
@@ -414,6 +461,7 @@ struct Engine {
       a.tau_l1 = (float)(step * cfg.lambda_l1);
       a.tau_tv = (float)(step * cfg.lambda_tv);
       a.lr_tv = a.tau_tv > 0.f ? (float)(1.0 / (8.0 * (step * cfg.lambda_tv))) : 0.f;
+      a.real_mode = cfg.real_nonnegative ? 1 : 0;
       HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzl, 1), s));
       if ((rc = prox_step(a, s))) return rc;
       if ((rc = read_scalars(s))) return rc;
@@ -440,6 +488,8 @@ struct Engine {
       out.step = step;
       out.ip = h_scal[SC_IP];
       out.dx2 = h_scal[SC_DX2];
+      // complex: lam1 sum|x| + lamTV (TV re + TV im); real engine: lam1 sum x + lamTV TV(x)
+      // (x >= 0 and Im = 0 there, so the same two sums; solver.py:146-151 / 212-216)
       out.pen = cfg.lambda_l1 * h_scal[SC_L1] + (cfg.lambda_tv > 0 ? cfg.lambda_tv * h_scal[SC_TV] : 0.0);
       if (cfg.step_policy != HOLO_POLICY_BACKTRACKING) return HOLO_OK;
       // Sufficient-decrease test of solver.py:324-326.  With ||A||^2 = nz the
@@ -505,6 +555,9 @@ struct Engine {
     double step;
     if (cfg.step_size > 0) {
       step = cfg.step_size;
+    } else if (cfg.real_nonnegative) {
+      return fail(HOLO_ERR_INVALID, "real_nonnegative needs step_size (the reference's power-iteration estimate; "
+                                    "see holo_power_iteration)");
     } else {
       const double sigma2 = (double)geom.nz;
       step = sigma2 > 0 ? 1.0 / (2.0 * sigma2) : 1.0;
@@ -687,10 +740,14 @@ int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end) {
   return HOLO_OK;
 }
 
-int holo_operator_norm(holo_handle* h, double* sigma2) {
-  if (!h || !sigma2) return fail(HOLO_ERR_INVALID, "null argument");
-  *sigma2 = h->e.plan.any_propagating ? (double)h->e.geom.nz : 0.0;
-  return HOLO_OK;
+int holo_operator_norm(holo_handle* h, int32_t real, double* sigma2) {
+  GUARD_HANDLE(h);
+  if (!sigma2) return fail(HOLO_ERR_INVALID, "null argument");
+  if (!real) {
+    *sigma2 = h->e.plan.any_propagating ? (double)h->e.geom.nz : 0.0;
+    return HOLO_OK;
+  }
+  TRY({ return h->e.real_opnorm_value(*sigma2, h->e.stream); })
 }
 
 int holo_solve_device(holo_handle* h, const double* b_dev, const holo_solver_config* cfg, holo_report* rep,
@@ -910,11 +967,10 @@ int holo_profile_read(holo_handle* h, int32_t* n, char* names, double* ms, int64
 
 int64_t holo_launch_count(void) { return holo::launch_count(); }
 
-int holo_power_iteration(holo_handle* h, int iters, uint64_t seed, double* sigma2) {
-  (void)iters;
-  (void)seed;
-  if (!h || !sigma2) return fail(HOLO_ERR_INVALID, "null argument");
-  return fail(HOLO_ERR_UNSUPPORTED, "power iteration not built yet");
+int holo_power_iteration(holo_handle* h, const void* v0, int32_t iters, int32_t real, double* sigma2, void* stream) {
+  GUARD_HANDLE(h);
+  if (!v0 || !sigma2 || iters < 1) return fail(HOLO_ERR_INVALID, "bad argument");
+  TRY({ return h->e.power_iteration((const float2*)v0, iters, real != 0, *sigma2, h->e.st(stream)); })
 }
 
 }  // extern "C"

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kSensorThreads) k_sensor(const float2* __restr
     const bool m = mask[p] != 0;
     // Re-part projection of the masked spectrum: FFT(Re IFFT(mS)) = m (S(f) + conj S(-f)) / 2
     float2 r = m ? make_float2(0.5f * (s1.x + s2.x), 0.5f * (s1.y - s2.y)) : czero();
-    r = csub(r, B[p]);
+    if (B) r = csub(r, B[p]);
     acc[0] += (double)r.x * r.x + (double)r.y * r.y;
     if (Rout) Rout[p] = m ? r : czero();
   }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
       }
       if (a.grad) {
         const float2 gg = a.grad[g];
-        y = make_float2(fmaf(-a.step, gg.x, y.x), fmaf(-a.step, gg.y, y.y));
+        y = make_float2(fmaf(-a.step, gg.x, y.x), a.real_mode ? y.y : fmaf(-a.step, gg.y, y.y));
       }
       vr[m] = y.x;
       vi[m] = y.y;
@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     }
     if (force & 1u) wr = vr[m];
     if (force & 2u) wi = vi[m];
-    if (a.tau_l1 > 0.f) {
+    if (a.real_mode) {
+      wr = fmaxf(wr - a.tau_l1, 0.f);  // solver.py:208-210: max(w - tau, 0)
+      wi = 0.f;
+    } else if (a.tau_l1 > 0.f) {
       const float mag = hypotf(wr, wi);
       if (mag > a.tau_l1) {
         const float gscale = 1.f - a.tau_l1 / mag;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     const float dxr = xr - y.x, dxi = xi - y.y;
     if (a.grad) {
       const float2 gg = a.grad[g];
-      acc[PT_IP] += (double)gg.x * dxr + (double)gg.y * dxi;
+      acc[PT_IP] += (double)gg.x * dxr + (a.real_mode ? 0.0 : (double)gg.y * dxi);
     }
     acc[PT_DX2] += (double)dxr * dxr + (double)dxi * dxi;
     a.xnew[g] = make_float2(xr, xi);
@@ -595,6 +598,58 @@ __global__ void k_spec_combine(const float2* __restrict__ Sa, const float2* __re
     float2 s = cscale(Sa[p], ca);
     if (Sb) s = cadd(s, cscale(Sb[p], cb));
     out[p] = s;
+  }
+}
+
+// per pixel: sum_k cos^2(2 pi (A + k B)) for the propagating band; block max
+__global__ void __launch_bounds__(256) k_real_opnorm(const ulonglong2* __restrict__ tab, const uint8_t* __restrict__ mask,
+                                                     const float2* __restrict__ circg, long long P, int nz,
+                                                     double* __restrict__ part) {
+  __shared__ float2 circ[256];
+  circ[threadIdx.x] = circg[threadIdx.x];
+  __syncthreads();
+  double best = 0.0;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    if (!mask[p]) continue;
+    double acc = 0.0;
+    for (int k = 0; k < nz; ++k) {
+      const float c = cis_cycles(plane_phase(tab[p], k), circ).x;
+      acc += (double)c * c;
+    }
+    best = fmax(best, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_down_sync(0xffffffffu, best, o));
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < 8; ++i) m = fmax(m, red[i]);
+    part[blockIdx.x] = m;
+  }
+}
+
+__global__ void k_max_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) m = fmax(m, part[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) *out = m;
+}
+
+__global__ void __launch_bounds__(256) k_vol_norm2(const float2* __restrict__ x, long long n, double* __restrict__ part) {
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float2 v = x[i];
+    acc[0] += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  block_sum<1, 256>(acc, part + blockIdx.x);
+}
+
+__global__ void k_vol_rescale(float2* __restrict__ x, long long n, const double* __restrict__ nrm2, int real) {
+  const float sc = nrm2 ? (float)(1.0 / sqrt(*nrm2)) : 1.f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float2 v = x[i];
+    x[i] = make_float2(v.x * sc, real ? 0.f : v.y * sc);
   }
 }
 
@@ -934,6 +989,33 @@ cudaError_t transfer_stack(const Plan& p, int k0, int k1, bool conj, float2* out
 cudaError_t spec_combine(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, float2* out,
                          cudaStream_t s) {
   k_spec_combine<<<grid_for(p.P, kEltThreads), kEltThreads, 0, s>>>(Sa, Sb, ca, cb, out, p.P);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t real_opnorm(const Plan& p, int nz, double* d_out, cudaStream_t s) {
+  const int nb = 148 * 2;
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, sizeof(double) * nb, s);
+  if (e) return e;
+  k_real_opnorm<<<nb, 256, 0, s>>>(p.phase, p.mask, p.circle, p.P, nz, part);
+  COUNT_LAUNCH(1);
+  k_max_final<<<1, 32, 0, s>>>(part, nb, d_out);
+  COUNT_LAUNCH(1);
+  cudaFreeAsync(part, s);
+  return cudaGetLastError();
+}
+
+int vol_norm2_blocks(long long n) { return grid_for(n, 256, 148 * 4); }
+
+cudaError_t vol_norm2(const float2* x, long long n, double* part, cudaStream_t s) {
+  k_vol_norm2<<<vol_norm2_blocks(n), 256, 0, s>>>(x, n, part);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+cudaError_t vol_rescale(float2* x, long long n, const double* nrm2, int real, cudaStream_t s) {
+  k_vol_rescale<<<grid_for(n, 256), 256, 0, s>>>(x, n, nrm2, real);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

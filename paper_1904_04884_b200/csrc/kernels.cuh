@@ -32,6 +32,7 @@ struct ProxArgs {
   int ny = 0, nx = 0, nplanes = 0;
   float beta = 0.f, step = 0.f;  // y = (1+beta) x - beta xp ; v = y - step * grad
   float tau_l1 = 0.f, tau_tv = 0.f, lr_tv = 0.f;
+  int real_mode = 0;  // real-nonnegative engine: Re(grad) only, x = max(w - tau_l1, 0), Im = 0
   int inner = 0, halo = 0, tile = 0, tiles_x = 0, tiles_per_plane = 0;
   int kind = 0;  // 0: generic tile kernel, 1: 64x64 register-strip kernel
   const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule (device)
@@ -96,6 +97,14 @@ cudaError_t transfer_stack(const Plan& p, int k0, int k1, bool conj, float2* out
 // S_out = ca * Sa + cb * Sb (elementwise)
 cudaError_t spec_combine(const Plan& p, const float2* Sa, const float2* Sb, float ca, float cb, float2* out,
                          cudaStream_t s);
+
+// ||A_real||^2 = max_f sum_k cos^2(phase_k(f)) over the propagating band (real engine)
+cudaError_t real_opnorm(const Plan& p, int nz, double* d_out, cudaStream_t s);
+// sum |x|^2 over n complex elements -> per-block partials (returns #blocks)
+int vol_norm2_blocks(long long n);
+cudaError_t vol_norm2(const float2* x, long long n, double* part, cudaStream_t s);
+// x = scale * (real ? (Re x, 0) : x), scale read from device (1/sqrt(*nrm2)) or 1 if null
+cudaError_t vol_rescale(float2* x, long long n, const double* nrm2, int real, cudaStream_t s);
 
 // COO export: count nonzeros per chunk, then compact in row-major order.
 int coo_chunks(long long P, int nplanes);

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
         y1 = fma2(cb, y1, mul2(cm, hi2(o)));
       }
       if (a.grad) {
-        const float4 gg = *reinterpret_cast<const float4*>(a.grad + g);
+        float4 gg = *reinterpret_cast<const float4*>(a.grad + g);
+        if (a.real_mode) gg.y = gg.w = 0.f;  // real engine: Re(grad) only
         y0 = fma2(cs, lo2(gg), y0);
         y1 = fma2(cs, hi2(gg), y1);
       }
@@ -285,6 +286,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
     for (int k = 0; k < 2; ++k) {
       const float wr = (force & 1u) ? v[s][k].x : rp[s][k].x;
       const float wi = (force & 2u) ? v[s][k].y : rp[s][k].y;
+      if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
+        p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
+        continue;
+      }
       const float n2 = fmaf(wr, wr, wi * wi);
       const float shrink = 1.f - tl * rsqrt_a(n2);
       const float gsc = (tl > 0.f) ? ((n2 > tl * tl) ? shrink : 0.f) : 1.f;
@@ -315,6 +320,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
       }
       float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
       if (a.grad) gr4 = *reinterpret_cast<const float4*>(a.grad + g);
+      if (a.real_mode) gr4.y = gr4.w = 0.f;
       const float2 gr[2] = {lo2(gr4), hi2(gr4)};
 #pragma unroll
       for (int k = 0; k < 2; ++k) {

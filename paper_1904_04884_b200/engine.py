@@ -67,9 +67,19 @@ class HoloEngine:
             pass
 
     # ------------------------------------------------------------ solver ---
-    def operator_norm(self) -> float:
+    def operator_norm(self, real: bool = False) -> float:
+        """Exact ||A||^2 (complex engine: nz; real engine: max_f sum_k cos^2)."""
         out = ctypes.c_double()
-        nat.check(self.lib.holo_operator_norm(self.h, ctypes.byref(out)))
+        nat.check(self.lib.holo_operator_norm(self.h, int(real), ctypes.byref(out)), "holo_operator_norm")
+        return out.value
+
+    def power_iteration(self, v0, iters: int = 10, real: bool = False) -> float:
+        """solver.py:225-247 on the GPU from the given unit-norm start volume (local planes)."""
+        torch = _torch()
+        v = torch.as_tensor(np.asarray(v0, dtype=np.complex64)).to(f"cuda:{self.device}").contiguous()
+        out = ctypes.c_double()
+        nat.check(self.lib.holo_power_iteration(self.h, ctypes.c_void_p(v.data_ptr()), int(iters), int(real),
+                                                ctypes.byref(out), _stream_ptr(torch)), "holo_power_iteration")
         return out.value
 
     def solve(self, b, cfg: nat.SolverConfig, stream=None):

@@ -9,8 +9,11 @@ Differences a caller can observe (documented in DESIGN.md):
     ``cfg.dtype`` says (the north-star parity bar is rel-L2 <= 1e-4 in fp32);
   * ``dense_plane_budget`` is accepted and ignored: the whole volume is
     resident in HBM (it only bounded host memory in the reference);
-  * ``real_nonnegative=True`` (the half-spectrum engine) is not built yet and
-    raises ``NotImplementedError``.
+  * ``real_nonnegative=True`` runs the same complex kernels restricted to real
+    volumes (the real engine's operators are the complex ones on real x, with
+    Re() of the adjoint), not the reference's half-spectrum rfft layout; its
+    step estimate replays the reference's power iteration (same
+    ``default_rng(0)`` start vector, generated on the host) on the GPU.
 """
 
 from __future__ import annotations
@@ -91,31 +94,44 @@ class DivergenceError(RuntimeError):
         self.report = report
 
 
-def native_config(cfg: SolverConfig) -> nat.SolverConfig:
+def native_config(cfg: SolverConfig, step_size: float | None = None) -> nat.SolverConfig:
     """SolverConfig -> the C struct of include/holo_b200.h."""
-    if cfg.real_nonnegative:
-        raise NotImplementedError("real_nonnegative (half-spectrum) engine is not built for the B200 path yet")
     w = cfg.weights
+    step = cfg.step_size if cfg.step_size is not None else step_size
     return nat.SolverConfig(
         lambda_l1=float(w.lambda_l1), lambda_tv=float(w.lambda_tv), max_iters=int(cfg.max_iters),
         tv_inner_iters=int(cfg.tv_inner_iters), step_policy=nat.POLICY[cfg.step_policy],
-        step_size=float(cfg.step_size) if cfg.step_size is not None else -1.0, bt_shrink=float(cfg.bt_shrink),
-        stop_tol=float(cfg.stop_tol), log_objective=int(bool(cfg.log_objective)))
+        step_size=float(step) if step is not None else -1.0, bt_shrink=float(cfg.bt_shrink),
+        stop_tol=float(cfg.stop_tol), log_objective=int(bool(cfg.log_objective)),
+        real_nonnegative=int(bool(cfg.real_nonnegative)))
+
+
+def power_start(geom, seed: int = 0, real: bool = False) -> np.ndarray:
+    """The reference's unit-norm start vector (solver.py:231-237): default_rng(seed) normals."""
+    rng = np.random.default_rng(seed)
+    shape = (geom.nz,) + tuple(geom.plane_shape)
+    if real:
+        v = rng.standard_normal(shape)
+    else:
+        v = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    return v / np.linalg.norm(v)
 
 
 def estimate_operator_norm(geom, iters: int = 10, seed: int = 0, real: bool = False, dtype: str = "float64") -> float:
-    """||A||^2 of the complex engine (solver.py:225-247).
+    """||A||^2 estimate (solver.py:225-247).
 
-    A A^H = nz * (band-limit projector) for the angular-spectrum stack, so the
-    reference's power iteration converges to nz after one step (it returns
-    nz to ~1e-15).  The closed form is returned; tests check it against the
-    reference's value and the GPU power iteration.
+    Complex engine: A A^H = nz * (band-limit projector), so the reference's
+    power iteration converges to nz after one step (it returns nz to
+    ~1e-15); the closed form is returned.  Real engine: the 10-step power
+    iteration does NOT converge, so the reference's estimate is
+    replayed on the GPU from the identical start vector.
     """
-    del iters, seed, dtype
-    if real:
-        raise NotImplementedError("real_nonnegative operator norm is not built for the B200 path yet")
+    del dtype
     from .engine import session
-    return session(geom).operator_norm()
+    eng = session(geom)
+    if not real:
+        return eng.operator_norm(False)
+    return eng.power_iteration(power_start(geom, seed, True), iters, real=True)
 
 
 def _check_b(b, geom):
@@ -136,7 +152,11 @@ def fista(b: ComplexField2D, geom: VolumeGeometry, cfg: SolverConfig):
 
     t0 = time.perf_counter()
     bb = _check_b(b, geom)
-    ncfg = native_config(cfg)
+    step = None
+    if cfg.real_nonnegative and cfg.step_size is None:
+        s2 = estimate_operator_norm(geom, real=True, dtype=cfg.dtype)
+        step = 1.0 / (2.0 * s2) if s2 > 0 else 1.0
+    ncfg = native_config(cfg, step)
     eng = session(geom)
     code, rep, hist = eng.solve(bb, ncfg)
     per, rows, cols, vals = eng.export_coo()

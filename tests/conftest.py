@@ -46,11 +46,13 @@ def rel_l2(a, b):
 
 
 FISTA_CASES = ["fista_64", "fista_64_tvheavy", "fista_64_stall", "fista_64_backtrack", "fista_64_fixed_stop",
-               "fista_64_diverge", "fista_64_zero", "fista_128", "fista_c1"]
+               "fista_64_diverge", "fista_64_zero", "fista_128", "fista_c1",
+               "fista_64_real", "fista_64_real_tv", "fista_128_real"]
 
 
 def fista_kwargs(d):
     lam = d["lam"]
     step = float(d["step_in"])
     return dict(lam_l1=float(lam[0]), lam_tv=float(lam[1]), max_iters=int(d["iters"]), inner=int(d["inner"]),
-                policy=str(d["policy"]), step_size=None if step < 0 else step, stop_tol=float(d["stop_tol"]))
+                policy=str(d["policy"]), step_size=None if step < 0 else step, stop_tol=float(d["stop_tol"]),
+                real=bool(d["real"]) if "real" in d else False)

@@ -100,9 +100,9 @@ def prox_fixture():
 
 
 def fista_fixture(name, g, b, truth=None, lam=(0.5, 0.2), iters=20, inner=5, policy="backtracking",
-                  step=None, stop_tol=0.0, detect=True):
+                  step=None, stop_tol=0.0, detect=True, real=False):
     cfg = solver.SolverConfig(weights=RegularizerWeights(*lam), max_iters=iters, tv_inner_iters=inner,
-                              step_policy=policy, step_size=step, stop_tol=stop_tol)
+                              step_policy=policy, step_size=step, stop_tol=stop_tol, real_nonnegative=real)
     t0 = time.time()
     diverged = False
     try:
@@ -123,7 +123,7 @@ def fista_fixture(name, g, b, truth=None, lam=(0.5, 0.2), iters=20, inner=5, pol
          policy=np.array(policy), step_in=np.array(-1.0 if step is None else step), stop_tol=np.array(stop_tol),
          k=k, r=r, c=c, v=v, history=np.array(rep.objective), iterations=np.array(rep.iterations),
          step=np.array(rep.step_size), restarts=np.array(rep.restarts), diverged=np.array(diverged),
-         final_sparsity=np.array(rep.final_sparsity), ref_seconds=np.array(dt), **extra)
+         final_sparsity=np.array(rep.final_sparsity), ref_seconds=np.array(dt), real=np.array(real), **extra)
     print(f"  {name}: {dt:.1f}s  iters={rep.iterations} restarts={rep.restarts} nnz={vol.nnz} "
           f"div={diverged} dets={len(extra.get('detections', []))}")
 
@@ -156,6 +156,24 @@ def main():
         g128 = VolumeGeometry(128, 128, 32, PITCH, DZ, Z0, LAM)
         b128, t128 = hologram(g128, 20, 20e-6, 12)
         fista_fixture("fista_128", g128, b128, t128, iters=30)
+    if want("real"):
+        b64, t64 = hologram(g64, 8, 20e-6, 11)
+        fista_fixture("fista_64_real", g64, b64, iters=15, real=True)
+        fista_fixture("fista_64_real_tv", g64, b64, lam=(0.05, 0.5), iters=10, inner=20, real=True)
+        g128 = VolumeGeometry(128, 128, 32, PITCH, DZ, Z0, LAM)
+        b128, t128 = hologram(g128, 20, 20e-6, 12)
+        fista_fixture("fista_128_real", g128, b128, t128, iters=20, real=True)
+        gr = VolumeGeometry(64, 32, 6, PITCH, DZ, Z0, LAM)
+        rng = np.random.default_rng(4)
+        shp = (gr.nz, gr.ny, gr.nx)
+        dense = rng.standard_normal(shp) * (rng.random(shp) < 0.05)
+        vol = sparsevol.SparseVolume.from_dense_stack(dense, gr)
+        r = rng.standard_normal(gr.plane_shape)
+        eng = solver._RealEngine(gr, "float64")
+        save("ops_real", geom=geom_arr(gr), x=dense, r=r, forward=eng.forward_sparse(vol.planes, 4),
+             gradient=np.concatenate([gc for _, _, gc in eng.gradient_chunks(r, 4)]),
+             sigma2=np.array(solver.estimate_operator_norm(gr, real=True)),
+             sigma2_g64=np.array(solver.estimate_operator_norm(g64, real=True)))
     if want("c1") and not a.skip_c1:
         gc1 = VolumeGeometry(256, 256, 64, PITCH, DZ, Z0, LAM)
         bc1, tc1 = hologram(gc1, 50, 20e-6, 0)

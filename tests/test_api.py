@@ -33,8 +33,8 @@ def test_native_config_mapping():
     c = native_config(SolverConfig(weights=RegularizerWeights(0.3, 0.1), step_policy="fixed", step_size=0.25))
     assert (c.lambda_l1, c.lambda_tv, c.step_policy, c.step_size) == (0.3, 0.1, 1, 0.25)
     assert native_config(SolverConfig()).step_size == -1.0
-    with pytest.raises(NotImplementedError):
-        native_config(SolverConfig(real_nonnegative=True))
+    assert native_config(SolverConfig(real_nonnegative=True), 0.25).real_nonnegative == 1
+    assert native_config(SolverConfig(real_nonnegative=True), 0.25).step_size == 0.25
 
 
 def test_fista_shape_mismatch_raises_before_device_work():

@@ -47,5 +47,6 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(nat.Geometry) == 3 * 4 + 4 + 4 * 8  # int32 x3, pad, 4 doubles
     assert nat.Geometry.pitch.offset == 16
     assert nat.SolverConfig.step_size.offset == 32
+    assert nat.SolverConfig.real_nonnegative.offset == 60 and ctypes.sizeof(nat.SolverConfig) == 64
     assert nat.Report.step_size.offset == 24
     assert nat.Report.nnz.offset == 56

@@ -20,6 +20,17 @@ def test_operators_match_reference(name):
     assert rel_l2(2.0 * bp, d["gradient"]) < 1e-12
 
 
+def test_real_engine_operators_match_reference():
+    d = golden("ops_real")
+    g = geom_of(d["geom"])
+    assert rel_l2(O.real_forward(d["x"], g), d["forward"]) < 1e-12
+    assert rel_l2(2.0 * O.real_back_project(d["r"], g), d["gradient"]) < 1e-12
+    assert abs(O.power_norm(g, real=True) - float(d["sigma2"])) < 1e-9 * float(d["sigma2"])
+    # the real engine is the complex engine restricted to real volumes
+    assert rel_l2(O.sensor_forward(d["x"].astype(complex), g), d["forward"]) < 1e-12
+    assert rel_l2(O.back_project(d["r"], g).real, 0.5 * d["gradient"]) < 1e-12
+
+
 def test_power_iteration_matches_reference():
     d = golden("ops_a")
     g = geom_of(d["geom"])
