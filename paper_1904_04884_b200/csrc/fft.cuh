@@ -16,8 +16,9 @@
 //
 // Sign convention (numpy): forward X[k] = sum x[n] exp(-2 pi i nk/N); the
 // inverse uses +i and is NOT scaled here (callers fold 1/N into their
-// epilogue).  Twiddles come from a table tw[i] = exp(-2 pi i i/N) (fp64-exact
-// entries rounded to fp32) held in shared memory.
+// epilogue).  Twiddles come from a table tw[m] = (w, conj w), w = exp(-2 pi i
+// m/N) (fp64-exact entries rounded to fp32) held in shared memory, so a table
+// twiddle multiply is one FMUL2 + one FFMA2.
 #pragma once
 #include "common.cuh"
 
@@ -33,8 +34,43 @@ struct FftShape {
   static constexpr int PADN = N + N / 16 + (TPF >= 16 ? 2 : TPF);
 };
 
-HD int fft_pad(int i) { return i + (i >> 4); }
+// Twiddle tables are stored per pass as [r-1][kk] (kk = butterfly index mod
+// NS), so the lanes of a warp (consecutive kk) read consecutive entries:
+// conflict-free, or broadcast.  Entry = (w, conj w), w = exp(-2 pi i kk r/(NS R)).
+template <int N>
+struct TwLayout {
+  static constexpr int radix(int ns) { return ((N / ns) % 16 == 0) ? 16 : N / ns; }
+  // offset of the table of the pass whose product of earlier radices is ns
+  static constexpr int offset(int ns) {
+    int off = 0;
+    for (int s = 16; s < ns; s *= radix(s)) off += (radix(s) - 1) * s;
+    return off;
+  }
+  static constexpr int size() {
+    int off = 0;
+    if (N <= 16) return 1;
+    for (int s = 16; s < N; s *= radix(s)) off += (radix(s) - 1) * s;
+    return off;
+  }
+};
 
+HD int fft_pad(int i) { return i + (i >> 4); }
+// pad(i + d) - pad(i) for a compile-time d that is a multiple of 16 (any i >= 0)
+template <int D>
+struct PadStep {
+  static_assert(D % 16 == 0, "");
+  static constexpr int value = D + D / 16;
+};
+
+// Complex arithmetic on packed f32x2 pairs (FADD2/FMUL2/FFMA2); the (re, im)
+// swap below compiles to the .LO_HI operand selector, not a move.
+HD float2 swp(float2 a) { return make_float2(a.y, a.x); }
+
+// c + (-i) d  (forward)  or  c + (+i) d  (inverse):  one FFMA2
+template <bool INV>
+HD float2 add_ni(float2 c, float2 d) {
+  return fma2(swp(d), INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f), c);
+}
 // multiply by -i (forward) or +i (inverse)
 template <bool INV>
 HD float2 mul_ni(float2 a) {
@@ -44,18 +80,18 @@ HD float2 mul_ni(float2 a) {
 template <bool INV>
 HD void dft2(float2& a, float2& b) {
   const float2 t = a;
-  a = cadd(t, b);
-  b = csub(t, b);
+  a = add2(t, b);
+  b = sub2(t, b);
 }
 
 template <bool INV>
 HD void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
-  const float2 t0 = cadd(a0, a2), t1 = csub(a0, a2);
-  const float2 t2 = cadd(a1, a3), t3 = mul_ni<INV>(csub(a1, a3));
-  a0 = cadd(t0, t2);
-  a2 = csub(t0, t2);
-  a1 = cadd(t1, t3);
-  a3 = csub(t1, t3);
+  const float2 t0 = add2(a0, a2), t1 = sub2(a0, a2);
+  const float2 t2 = add2(a1, a3), t3 = sub2(a1, a3);
+  a0 = add2(t0, t2);
+  a2 = sub2(t0, t2);
+  a1 = add_ni<INV>(t1, t3);
+  a3 = add_ni<!INV>(t1, t3);
 }
 
 // x * exp(-/+ 2 pi i e / 16), e in [0, 16) compile-time
@@ -78,9 +114,20 @@ HD float2 rot16(float2 x) {
     constexpr float sn = (ee == 1 || ee == 7) ? S1 : (ee == 2 || ee == 6) ? R2 : (ee == 3 || ee == 5) ? C1
                        : (ee == 9 || ee == 15) ? -S1 : (ee == 10 || ee == 14) ? -R2 : -C1;
     // forward: multiply by (cs, -sn); inverse: (cs, +sn)
+    //   x (cs + i s) = x * cs + swap(x) * (-s, s)
     constexpr float s = INV ? sn : -sn;
-    return make_float2(fmaf(x.x, cs, -x.y * s), fmaf(x.x, s, x.y * cs));
+    return fma2(swp(x), make_float2(-s, s), mul2(x, make_float2(cs, cs)));
   }
+}
+
+// a * w (forward) or a * conj(w) (inverse) with the table entry t = (w, conj w):
+//   a w      = a.x (w)      + a.y swap(conj w)
+//   a conj w = a.x (conj w) + a.y swap(w)
+template <bool INV>
+HD float2 twiddle(float2 a, float4 t) {
+  const float2 w = make_float2(t.x, t.y), cw = make_float2(t.z, t.w);
+  return INV ? fma2(make_float2(a.y, a.y), swp(w), mul2(make_float2(a.x, a.x), cw))
+             : fma2(make_float2(a.y, a.y), swp(cw), mul2(make_float2(a.x, a.x), w));
 }
 
 template <int R, bool INV>
@@ -101,10 +148,10 @@ struct Dft<8, INV> {
     dft4<INV>(a[1], a[3], a[5], a[7]);
     float2 o1 = rot16<INV, 2>(a[3]), o2 = rot16<INV, 4>(a[5]), o3 = rot16<INV, 6>(a[7]);
     float2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6], o0 = a[1];
-    a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
-    a[1] = cadd(e1, o1); a[5] = csub(e1, o1);
-    a[2] = cadd(e2, o2); a[6] = csub(e2, o2);
-    a[3] = cadd(e3, o3); a[7] = csub(e3, o3);
+    a[0] = add2(e0, o0); a[4] = sub2(e0, o0);
+    a[1] = add2(e1, o1); a[5] = sub2(e1, o1);
+    a[2] = add2(e2, o2); a[6] = sub2(e2, o2);
+    a[3] = add2(e3, o3); a[7] = sub2(e3, o3);
   }
 };
 // 16 = 4 x 4: DFT4 over a (stride 4), twiddle w16^(b*k1), DFT4 over b, transpose.
@@ -138,12 +185,18 @@ struct Dft<16, INV> {
 
 // One Stockham pass of radix R with NS = product of earlier radices.
 template <int N, int R, int NS, bool INV, bool FIRST, bool LAST>
-HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float2* __restrict__ tw) {
+HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
   constexpr int E = FftShape<N>::E, TPF = FftShape<N>::TPF, BPT = E / R;
   static_assert(E % R == 0, "radix must divide E");
   if constexpr (!FIRST) {
+    if constexpr (TPF % 16 == 0) {
+      const float2* rp = buf + fft_pad(j) * S;  // one address, immediate offsets
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = buf[fft_pad(j + m * TPF) * S];
+      for (int m = 0; m < E; ++m) v[m] = rp[m * PadStep<TPF>::value * S];
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) v[m] = buf[fft_pad(j + m * TPF) * S];
+    }
     if constexpr (!LAST) __syncthreads();  // everyone has read before anyone writes
   } else if constexpr (!LAST) {
     __syncthreads();  // buffer may still be read by a previous transform's last pass
@@ -157,10 +210,13 @@ HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const f
     if constexpr (NS > 1) {
       const int kk = b % NS;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        float2 w = tw[kk * r * (N / (NS * R))];
-        if (INV) w.y = -w.y;
-        a[r] = cmul(a[r], w);
+      const float4* tp = tw + TwLayout<N>::offset(NS) + kk;
+      // groups of 4 twiddles: bounds the 4-register table entries in flight
+#pragma unroll
+      for (int r0 = 1; r0 < R; r0 += 4) {
+#pragma unroll
+        for (int r = r0; r < r0 + 4 && r < R; ++r) a[r] = twiddle<INV>(a[r], tp[(r - 1) * NS]);
+        if (R > 4) asm volatile("" ::: "memory");
       }
     }
     Dft<R, INV>::run(a);
@@ -169,15 +225,24 @@ HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const f
       for (int r = 0; r < R; ++r) v[s + r * BPT] = a[r];
     } else {
       const int base = (b / NS) * NS * R + (b % NS);
+      float2* wp = buf + fft_pad(base) * S;
+      if constexpr (NS % 16 == 0) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[fft_pad(base + r * NS) * S] = a[r];
+        for (int r = 0; r < R; ++r) wp[r * PadStep<NS>::value * S] = a[r];
+      } else if constexpr (NS == 1 && R == 16) {  // base = 16 b: pad(base + r) = pad(base) + r
+#pragma unroll
+        for (int r = 0; r < R; ++r) wp[r * S] = a[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[fft_pad(base + r * NS) * S] = a[r];
+      }
     }
   }
   if constexpr (!LAST) __syncthreads();
 }
 
 template <int N, int NS, bool INV, bool FIRST>
-HD void fft_passes(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float2* __restrict__ tw) {
+HD void fft_passes(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
   constexpr int REM = N / NS;
   constexpr int R = (REM % 16 == 0) ? 16 : REM;
   constexpr bool LAST = (NS * R == N);
@@ -188,7 +253,7 @@ HD void fft_passes(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const
 // Full length-N transform of the line held by the TPF threads j=0..TPF-1.
 // Contains __syncthreads(): every thread of the block must call it.
 template <int N, bool INV>
-HD void fft_line(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float2* __restrict__ tw) {
+HD void fft_line(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
   fft_passes<N, 1, INV, true>(v, j, buf, S, tw);
 }
 

@@ -51,12 +51,23 @@ inline int col_width(int ny) { return ny >= 4096 ? 4 : 8; }
 
 // ------------------------------------------------------------ K1 tables ----
 
-__global__ void k_twiddles(float2* tw, int n) {
-  int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m < n) {
-    double s, c;
-    sincospi(-2.0 * (double)m / (double)n, &s, &c);
-    tw[m] = make_float2((float)c, (float)s);
+// per-pass twiddle tables (TwLayout): entry (r-1)*NS + kk of the pass with
+// product-of-earlier-radices NS holds w = exp(-2 pi i kk r / (NS R)) as (w, conj w)
+template <int N>
+__global__ void k_twiddles(float4* tw) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= TwLayout<N>::size()) return;
+  int off = 0;
+  for (int ns = 16; ns < N; ns *= TwLayout<N>::radix(ns)) {
+    const int R = TwLayout<N>::radix(ns);
+    if (e < off + (R - 1) * ns) {
+      const int r = 1 + (e - off) / ns, kk = (e - off) % ns;
+      double sn, cs;
+      sincospi(-2.0 * (double)kk * r / ((double)ns * R), &sn, &cs);
+      tw[e] = make_float4((float)cs, (float)sn, (float)cs, (float)-sn);
+      return;
+    }
+    off += (R - 1) * ns;
   }
 }
 
@@ -73,15 +84,16 @@ __device__ double fftfreq(int i, int n, double d) {
   return (double)k * (1.0 / ((double)n * d));
 }
 
-__device__ uint64_t frac_to_u64(double a) {
+// frac(a) rounded to `bits` bits, as an integer in [0, 2^bits)
+__device__ uint64_t frac_bits(double a, int bits) {
   double f = a - floor(a);
-  if (f >= 1.0) f = 0.0;
-  return __double2ull_rn(f * 18446744073709551616.0 * 0.5) << 1;  // 63-bit precision, avoids overflow
+  uint64_t v = __double2ull_rn(f * (double)(1ull << bits));
+  return v & ((1ull << bits) - 1ull);  // f rounding up to 1.0 wraps to 0 (same phase)
 }
 
 // Phase cycles of H(z) at a pixel: (z / lam) * sqrt(1 - (lam fx)^2 - (lam fy)^2)
 // (optics.py:98-116).  Evanescent pixels (arg < 0) get mask 0 and phase 0.
-__global__ void k_phase(ulonglong2* tab, uint8_t* mask, int ny, int nx, double pitch, double lam, double z0,
+__global__ void k_phase(uint64_t* tab, uint8_t* mask, int ny, int nx, double pitch, double lam, double z0,
                         double dz) {
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (long long)ny * nx) return;
@@ -91,7 +103,9 @@ __global__ void k_phase(ulonglong2* tab, uint8_t* mask, int ny, int nx, double p
   const double arg = 1.0 - ax * ax - ay * ay;
   const bool prop = arg >= 0.0;
   const double root = prop ? sqrt(arg) : 0.0;
-  tab[p] = make_ulonglong2(frac_to_u64((z0 / lam) * root), frac_to_u64((dz / lam) * root));
+  const uint64_t A = frac_bits((z0 / lam) * root, 64 - kPhaseBBits);
+  const uint64_t B = frac_bits((dz / lam) * root, kPhaseBBits);
+  tab[p] = (A << kPhaseBBits) | B;
   mask[p] = prop ? 1 : 0;
 }
 
@@ -99,28 +113,29 @@ __global__ void k_phase(ulonglong2* tab, uint8_t* mask, int ny, int nx, double p
 
 template <int N, bool INV>
 __global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
-                                                          long long nrows, float scale, const float2* __restrict__ twg) {
+                                                          long long nrows, float scale, const float4* __restrict__ twg) {
   using Sh = FftShape<N>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int RPC = kRowThreads / TPF;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* buf = smem + N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  float4* tw = reinterpret_cast<float4*>(smem);
+  float2* buf = smem + 2 * N;
+  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
   __syncthreads();
   const int lr = threadIdx.x / TPF, j = threadIdx.x % TPF;
   for (long long row0 = (long long)blockIdx.x * RPC; row0 < nrows; row0 += (long long)gridDim.x * RPC) {
     const long long row = row0 + lr;
     const bool active = row < nrows;
     float2 v[E];
-    const float2* src = in + row * N;
+    const float2* src = in + row * N + j;
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = active ? src[j + m * TPF] : czero();
+    for (int m = 0; m < E; ++m) v[m] = active ? src[m * TPF] : czero();
     fft_line<N, INV>(v, j, buf + lr * Sh::PADN, 1, tw);
     if (active) {
-      float2* dst = out + row * N;
+      float2* dst = out + row * N + j;
+      const float2 sc = splat2(scale);
 #pragma unroll
-      for (int m = 0; m < E; ++m) dst[j + m * TPF] = cscale(v[m], scale);
+      for (int m = 0; m < E; ++m) dst[m * TPF] = mul2(v[m], sc);
     }
   }
 }
@@ -133,54 +148,53 @@ __global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restri
 template <int N, bool INV, int C>
 __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fft_cols(const float2* __restrict__ in,
                                                                     float2* __restrict__ out, int nx, long long P,
-                                                                    float scale, const float2* __restrict__ twg) {
+                                                                    float scale, const float4* __restrict__ twg) {
   using Sh = FftShape<N>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* buf = smem + N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  float4* tw = reinterpret_cast<float4*>(smem);
+  float2* buf = smem + 2 * N;
+  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
-  const long long base = (long long)blockIdx.y * P + col;
+  const long long base = (long long)blockIdx.y * P + (long long)j * nx + col;
+  const long long st = (long long)TPF * nx;
   float2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = in[base + (long long)(j + m * TPF) * nx];
+  for (int m = 0; m < E; ++m) v[m] = in[base + m * st];
   fft_line<N, INV>(v, j, buf + c, C, tw);
 #pragma unroll
-  for (int m = 0; m < E; ++m) out[base + (long long)(j + m * TPF) * nx] = cscale(v[m], scale);
+  for (int m = 0; m < E; ++m) out[base + m * st] = cscale(v[m], scale);
 }
 
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
 template <int N, int C>
 __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_adj_cols(const float2* __restrict__ R,
                                                                     float2* __restrict__ out, int nx, long long P,
-                                                                    int k0, const ulonglong2* __restrict__ tab,
-                                                                    const float2* __restrict__ twg,
+                                                                    int k0, const uint64_t* __restrict__ tab,
+                                                                    const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
   using Sh = FftShape<N>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* circ = smem + N;
-  float2* buf = smem + N + 256;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  float4* tw = reinterpret_cast<float4*>(smem);
+  float2* circ = smem + 2 * N;
+  float2* buf = smem + 2 * N + 256;
+  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
   const int k = blockIdx.y;
+  const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
   float2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const long long p = (long long)(j + m * TPF) * nx + col;
-    v[m] = cmul(R[p], cis_cycles(plane_phase(tab[p], k0 + k), circ));
-  }
+  for (int m = 0; m < E; ++m) v[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ));
   fft_line<N, true>(v, j, buf + c, C, tw);
-  float2* dst = out + (long long)k * P + col;
+  float2* dst = out + (long long)k * P + p0;
 #pragma unroll
-  for (int m = 0; m < E; ++m) dst[(long long)(j + m * TPF) * nx] = v[m];
+  for (int m = 0; m < E; ++m) dst[m * st] = v[m];
 }
 
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
@@ -188,16 +202,16 @@ template <int N, int C>
 __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fwd_cols(const float2* __restrict__ in,
                                                                     float2* __restrict__ Spart, int nx, long long P,
                                                                     int nzl, int ppg, int k0,
-                                                                    const ulonglong2* __restrict__ tab,
-                                                                    const float2* __restrict__ twg,
+                                                                    const uint64_t* __restrict__ tab,
+                                                                    const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
   using Sh = FftShape<N>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* circ = smem + N;
-  float2* buf = smem + N + 256;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tw[i] = twg[i];
+  float4* tw = reinterpret_cast<float4*>(smem);
+  float2* circ = smem + 2 * N;
+  float2* buf = smem + 2 * N + 256;
+  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
@@ -206,21 +220,26 @@ __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fwd_cols(const float2*
   float2 acc[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
+  const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
   for (int k = kb; k < ke; ++k) {
     float2 v[E];
-    const float2* src = in + (long long)k * P + col;
+    const float2* src = in + (long long)k * P + p0;
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = src[(long long)(j + m * TPF) * nx];
+    for (int m = 0; m < E; ++m) v[m] = src[m * st];
     fft_line<N, false>(v, j, buf + c, C, tw);
+    // transfer multiply-accumulate in chunks of 4: bounds the table loads in
+    // flight (16 B each) so acc[] + v[] stay in registers
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const long long p = (long long)(j + m * TPF) * nx + col;
-      acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p], k0 + k), circ)));
+    for (int m0 = 0; m0 < E; m0 += 4) {
+#pragma unroll
+      for (int m = m0; m < m0 + 4 && m < E; ++m)
+        acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ)));
+      asm volatile("" ::: "memory");
     }
   }
-  float2* dst = Spart + (long long)blockIdx.y * P + col;
+  float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
-  for (int m = 0; m < E; ++m) dst[(long long)(j + m * TPF) * nx] = acc[m];
+  for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
 }
 
 __global__ void k_sum_groups(const float2* __restrict__ Spart, int groups, long long P, float2* __restrict__ S) {
@@ -580,7 +599,7 @@ __global__ void k_apply_mask(float2* __restrict__ spec, const uint8_t* __restric
     if (!mask[p % P]) spec[p] = czero();
 }
 
-__global__ void k_transfer(const ulonglong2* __restrict__ tab, const uint8_t* __restrict__ mask,
+__global__ void k_transfer(const uint64_t* __restrict__ tab, const uint8_t* __restrict__ mask,
                            const float2* __restrict__ circ, long long P, int k0, int nk, int conj,
                            float2* __restrict__ out) {
   const long long n = P * nk;
@@ -602,7 +621,7 @@ __global__ void k_spec_combine(const float2* __restrict__ Sa, const float2* __re
 }
 
 // per pixel: sum_k cos^2(2 pi (A + k B)) for the propagating band; block max
-__global__ void __launch_bounds__(256) k_real_opnorm(const ulonglong2* __restrict__ tab, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(256) k_real_opnorm(const uint64_t* __restrict__ tab, const uint8_t* __restrict__ mask,
                                                      const float2* __restrict__ circg, long long P, int nz,
                                                      double* __restrict__ part) {
   __shared__ float2 circ[256];
@@ -746,15 +765,20 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
   p.pitch = pitch; p.dz = dz; p.z0 = z0; p.lam = lam;
   p.col_c = col_width(ny);
   cudaError_t e;
-  if ((e = cudaMalloc(&p.tw_x, sizeof(float2) * nx))) return e;
-  if ((e = cudaMalloc(&p.tw_y, sizeof(float2) * ny))) return e;
+  if ((e = cudaMalloc(&p.tw_x, sizeof(float4) * std::max(nx, 16)))) return e;
+  if ((e = cudaMalloc(&p.tw_y, sizeof(float4) * std::max(ny, 16)))) return e;
   if ((e = cudaMalloc(&p.circle, sizeof(float2) * 256))) return e;
-  if ((e = cudaMalloc(&p.phase, sizeof(ulonglong2) * p.P))) return e;
+  if ((e = cudaMalloc(&p.phase, sizeof(uint64_t) * p.P))) return e;
   if ((e = cudaMalloc(&p.mask, p.P))) return e;
-  k_twiddles<<<(nx + 255) / 256, 256, 0, s>>>(p.tw_x, nx);
-  COUNT_LAUNCH(1);
-  k_twiddles<<<(ny + 255) / 256, 256, 0, s>>>(p.tw_y, ny);
-  COUNT_LAUNCH(1);
+  dispatch_n(nx, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    k_twiddles<N><<<(TwLayout<N>::size() + 255) / 256, 256, 0, s>>>(p.tw_x);
+  });
+  dispatch_n(ny, [&](auto nc) {
+    constexpr int N = decltype(nc)::value;
+    k_twiddles<N><<<(TwLayout<N>::size() + 255) / 256, 256, 0, s>>>(p.tw_y);
+  });
+  COUNT_LAUNCH(2);
   k_circle<<<1, 256, 0, s>>>(p.circle);
   COUNT_LAUNCH(1);
   k_phase<<<(int)((p.P + 255) / 256), 256, 0, s>>>(p.phase, p.mask, ny, nx, pitch, lam, z0, dz);
@@ -767,7 +791,8 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
 
 void plan_free(Plan& p) {
   cudaFree(p.tw_x); cudaFree(p.tw_y); cudaFree(p.circle); cudaFree(p.phase); cudaFree(p.mask);
-  p.tw_x = p.tw_y = p.circle = nullptr;
+  p.tw_x = p.tw_y = nullptr;
+  p.circle = nullptr;
   p.phase = nullptr;
   p.mask = nullptr;
 }
@@ -785,7 +810,7 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
     constexpr int N = decltype(nc)::value;
     using Sh = FftShape<N>;
     constexpr int RPC = kRowThreads / Sh::TPF;
-    const size_t smem = sizeof(float2) * (N + (size_t)RPC * Sh::PADN);
+    const size_t smem = sizeof(float2) * (2 * N + (size_t)RPC * Sh::PADN);
     const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
     if (inverse) {
       err = set_smem(k_fft_rows<N, true>, smem);
@@ -803,7 +828,7 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
 
 template <int N, int C>
 static size_t col_smem(int extra) {
-  return sizeof(float2) * (N + extra + (size_t)(N + N / 16) * C);
+  return sizeof(float2) * (2 * N + extra + (size_t)(N + N / 16) * C);
 }
 
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
@@ -846,8 +871,8 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
 }
 
 int fwd_groups(const Plan& p, int nzl) {
-  const int tiles = std::max(1, p.nx / p.col_c);
-  int g = (4 * 148 + tiles - 1) / tiles;
+  const int tiles = std::max(1, p.nx / 4);
+  int g = (16 * 148 + tiles - 1) / tiles;  // ~8 waves of 2 CTAs/SM: small tail
   g = std::max(1, std::min(g, nzl));
   return std::min(g, 64);
 }
@@ -857,7 +882,7 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
-    constexpr int C = N >= 4096 ? 4 : 8;
+    constexpr int C = 4;  // acc[] + v[] per thread: 256-thread CTAs keep them in registers
     constexpr int NT = C * FftShape<N>::TPF;
     const size_t smem = col_smem<N, C>(256);
     dim3 grid(p.nx / C, groups);

@@ -11,10 +11,10 @@ struct Plan {
   long long P = 0;             // ny * nx
   double pitch = 0, dz = 0, z0 = 0, lam = 0;
   int col_c = 8;                // interleaved columns per column-pass CTA
-  float2* tw_x = nullptr;       // exp(-2 pi i m / nx), m < nx
-  float2* tw_y = nullptr;       // exp(-2 pi i m / ny)
+  float4* tw_x = nullptr;       // (w, conj w), w = exp(-2 pi i m / nx), m < nx
+  float4* tw_y = nullptr;       // same for ny
   float2* circle = nullptr;     // exp(2 pi i m / 256)
-  ulonglong2* phase = nullptr;  // per pixel (frac(z0 q), frac(dz q)) as 64-bit cycle fractions
+  uint64_t* phase = nullptr;    // per pixel packed (frac(z0 q), frac(dz q)) cycle fractions (plane_phase)
   uint8_t* mask = nullptr;      // per pixel 1 = propagating (arg >= 0)
   int any_propagating = 0;
 };

@@ -21,6 +21,8 @@
 // Loads/stores are 16-byte (two complex64) per lane, 512 B per warp per row.
 // The FGP A/B half-steps are fused into one sweep down the band per
 // iteration, and the (re, im) arithmetic is packed FADD2/FMUL2/FFMA2.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -61,21 +63,54 @@ HD void project(float2& pn, float2& qn) {
   qn = mul2(qn, sc);
 }
 
-template <bool TV>
-__global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
-  const int plane = blockIdx.y, tile = blockIdx.x;
-  uint32_t force = 0;
-  if (a.force) {
-    force = a.force[plane];
-    if (!force) return;  // fix-up pass: only planes whose guard fired
-  }
-  __shared__ Bands sm;
-  const int TI = a.tile, H = a.halo;
+struct TileGeom {
+  int i0, i1, j0, j1, ri0, rj0;
+};
+
+HD TileGeom tile_geom(const ProxArgs& a, int tile) {
+  TileGeom t;
   const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-  const int i0 = ty * TI, j0 = tx * TI;
-  const int i1 = min(a.ny, i0 + TI), j1 = min(a.nx, j0 + TI);
-  const int ri0 = min(max(i0 - H, 0), a.ny - RH);  // region clamped into the plane
-  const int rj0 = min(max(j0 - H, 0), a.nx - RW);
+  t.i0 = ty * a.tile;
+  t.j0 = tx * a.tile;
+  t.i1 = min(a.ny, t.i0 + a.tile);
+  t.j1 = min(a.nx, t.j0 + a.tile);
+  t.ri0 = min(max(t.i0 - a.halo, 0), a.ny - RH);  // region clamped into the plane
+  t.rj0 = min(max(t.j0 - a.halo, 0), a.nx - RW);
+  return t;
+}
+
+HD long long strip_base(const ProxArgs& a, int plane, const TileGeom& t) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return (long long)plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
+}
+
+// per-thread prefetch slots: pre[(arr * SR + s) * NT + tid], arr = 0 x, 1 x_prev, 2 grad
+HD void cp_async16(float4* smem_dst, const float2* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+HD void prefetch_tile(const ProxArgs& a, float4* pre, int work) {
+  const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
+  const long long g0 = strip_base(a, plane, tile_geom(a, tile));
+#pragma unroll
+  for (int s = 0; s < SR; ++s) {
+    const long long g = g0 + (long long)s * a.nx;
+    cp_async16(pre + (0 * SR + s) * NT + threadIdx.x, a.x + g);
+    if (a.beta != 0.f) cp_async16(pre + (1 * SR + s) * NT + threadIdx.x, a.xp + g);
+    if (a.grad) cp_async16(pre + (2 * SR + s) * NT + threadIdx.x, a.grad + g);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// One 64x64 region.  Inputs come from this thread's prefetch slots; the
+// prefetch of `next_work` (if >= 0) is issued as soon as the slots are read.
+template <bool TV>
+__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, float4* pre_next, int work,
+                                          int next_work) {
+  const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
+  const uint32_t force = a.force ? a.force[plane] : 0u;
+  const TileGeom tg = tile_geom(a, tile);
+  const int i0 = tg.i0, i1 = tg.i1, j0 = tg.j0, j1 = tg.j1, ri0 = tg.ri0, rj0 = tg.rj0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool lane0 = lane == 0, lane31 = lane == 31;
   const int r0 = w * SR;
@@ -90,23 +125,23 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
     for (int k = 0; k < 2; ++k)
       if (rowInt && gj + k >= j0 && gj + k < j1) mInt |= 1u << (2 * s + k);
   }
-  const long long g0 = (long long)plane * a.P + (long long)(ri0 + r0) * a.nx + gj;
+  const long long g0 = strip_base(a, plane, tg);
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
   {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // my slots for this tile have landed
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
-      const long long g = g0 + (long long)s * a.nx;
-      float4 y = *reinterpret_cast<const float4*>(a.x + g);
+      const float4 y = pre[(0 * SR + s) * NT + threadIdx.x];
       float2 y0 = lo2(y), y1 = hi2(y);
       if (a.beta != 0.f) {
-        const float4 o = *reinterpret_cast<const float4*>(a.xp + g);
+        const float4 o = pre[(1 * SR + s) * NT + threadIdx.x];
         y0 = fma2(cb, y0, mul2(cm, lo2(o)));
         y1 = fma2(cb, y1, mul2(cm, hi2(o)));
       }
       if (a.grad) {
-        float4 gg = *reinterpret_cast<const float4*>(a.grad + g);
+        float4 gg = pre[(2 * SR + s) * NT + threadIdx.x];
         if (a.real_mode) gg.y = gg.w = 0.f;  // real engine: Re(grad) only
         y0 = fma2(cs, lo2(gg), y0);
         y1 = fma2(cs, hi2(gg), y1);
@@ -114,6 +149,9 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
       v[s][0] = y0;
       v[s][1] = y1;
     }
+    // the slots are free again (each thread only reads its own): overlap the
+    // next region's HBM reads with this region's FGP iterations
+    if (next_work >= 0) prefetch_tile(a, pre_next, next_work);
   }
 
   // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
@@ -311,15 +349,15 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
       const uint32_t rowbits = (mInt >> (2 * s)) & 3u;
       if (!rowbits) continue;
       const long long g = g0 + (long long)s * a.nx;
-      float4 y4 = *reinterpret_cast<const float4*>(a.x + g);
+      const float4 y4 = pre[(0 * SR + s) * NT + threadIdx.x];
       float2 y[2] = {lo2(y4), hi2(y4)};
       if (a.beta != 0.f) {
-        const float4 o = *reinterpret_cast<const float4*>(a.xp + g);
+        const float4 o = pre[(1 * SR + s) * NT + threadIdx.x];
         y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
         y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
       }
       float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.grad) gr4 = *reinterpret_cast<const float4*>(a.grad + g);
+      if (a.grad) gr4 = pre[(2 * SR + s) * NT + threadIdx.x];
       if (a.real_mode) gr4.y = gr4.w = 0.f;
       const float2 gr[2] = {lo2(gr4), hi2(gr4)};
 #pragma unroll
@@ -345,6 +383,29 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
 #pragma unroll
   for (int i = 0; i < kProxParts; ++i) accd[i] = (double)acc[i];
   block_sum<kProxParts, NT>(accd, a.part + ((long long)plane * a.tiles_per_plane + tile) * kProxParts);
+  __syncthreads();  // band buffers are reused by the next region
+}
+
+// Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
+// (fix-up pass: only regions of planes whose guard fired).
+template <bool TV>
+__global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
+  __shared__ Bands sm;
+  extern __shared__ float4 pre[];  // [2][3][SR][NT] double-buffered prefetch slots
+  const int total = a.tiles_per_plane * a.nplanes;
+  auto next_from = [&](int t) {
+    if (a.force)
+      while (t < total && !a.force[t / a.tiles_per_plane]) t += gridDim.x;
+    return t < total ? t : -1;
+  };
+  int work = next_from(blockIdx.x);
+  if (work < 0) return;
+  prefetch_tile(a, pre, work);
+  for (int buf = 0; work >= 0; buf ^= 1) {
+    const int nxt = next_from(work + gridDim.x);
+    prox_tile<TV>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+    work = nxt;
+  }
 }
 
 }  // namespace
@@ -375,11 +436,24 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
 }
 
 cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
-  dim3 grid(a.tiles_per_plane, a.nplanes);
-  if (a.tau_tv > 0.f)
-    k_prox_strip<true><<<grid, NT, 0, s>>>(a);
-  else
-    k_prox_strip<false><<<grid, NT, 0, s>>>(a);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = sizeof(float4) * 2 * 3 * SR * NT;
+  const long long total = (long long)a.tiles_per_plane * a.nplanes;
+  const int grid = (int)std::min<long long>(total, nsm);
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e;
+  if (a.tau_tv > 0.f) {
+    if ((e = cudaFuncSetAttribute(k_prox_strip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k_prox_strip<true><<<grid, NT, smem, s>>>(a);
+  } else {
+    if ((e = cudaFuncSetAttribute(k_prox_strip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    k_prox_strip<false><<<grid, NT, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
