@@ -1,7 +1,7 @@
 # Builds the sm_100a C-ABI library of the hot path (no GPU needed to compile).
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -DHOLO_WITH_NCCL --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -DHOLO_WITH_NCCL --expt-relaxed-constexpr $(EXTRA)
 SRC := paper_1904_04884_b200/csrc/kernels.cu paper_1904_04884_b200/csrc/prox_strip.cu paper_1904_04884_b200/csrc/engine.cu
 HDR := $(wildcard paper_1904_04884_b200/csrc/*.cuh) include/holo_b200.h
 LIB := paper_1904_04884_b200/libholo_b200.so

@@ -30,9 +30,12 @@ namespace holo {
 namespace {
 
 constexpr int RW = 64;  // region width: one warp, 2 columns per lane
-constexpr int SR = 4;   // rows per thread
-constexpr int NW = 16;  // warps = row bands
-constexpr int RH = SR * NW;
+constexpr int RH = 64;  // region height
+#ifndef HOLO_PROX_SR
+#define HOLO_PROX_SR 4
+#endif
+constexpr int SR = HOLO_PROX_SR;  // rows per thread (2: 1024 threads / 64 regs; 4: 512 threads / 128 regs)
+constexpr int NW = RH / SR;       // warps = row bands
 constexpr int NT = 32 * NW;
 
 struct Bands {
@@ -57,8 +60,8 @@ HD float2 norm_pair(float2 a, float2 b) {
 // (pn, qn) /= max(1, |(pn, qn)|) for each of the (re, im) parts
 HD void project(float2& pn, float2& qn) {
   const float2 n2 = fma2(pn, pn, mul2(qn, qn));
-  const float rx = rsqrt_a(n2.x), ry = rsqrt_a(n2.y);  // unconditional MUFU, then select
-  const float2 sc = make_float2(n2.x > 1.f ? rx : 1.f, n2.y > 1.f ? ry : 1.f);
+  // 1 / max(1, |.|) = rsqrt(max(1, |.|^2)); MUFU.RSQ(1) = 1 exactly
+  const float2 sc = make_float2(rsqrt_a(fmaxf(n2.x, 1.f)), rsqrt_a(fmaxf(n2.y, 1.f)));
   pn = mul2(pn, sc);
   qn = mul2(qn, sc);
 }
@@ -104,7 +107,13 @@ HD void prefetch_tile(const ProxArgs& a, float4* pre, int work) {
 
 // One 64x64 region.  Inputs come from this thread's prefetch slots; the
 // prefetch of `next_work` (if >= 0) is issued as soon as the slots are read.
-template <bool TV>
+// EDGE: the region touches the plane's left or right edge, so its outer
+// columns need the exact replicated-edge rule; otherwise they are garbage
+// zone and the lane-0 / lane-31 selects are skipped.
+// prefetch through shared memory only when the smem budget allows the double buffer
+constexpr bool PF = (SR >= 4);
+
+template <bool TV, bool EDGE>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, float4* pre_next, int work,
                                           int next_work) {
   const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
@@ -130,18 +139,19 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
   {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // my slots for this tile have landed
+    if (PF) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // my slots for this tile have landed
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
-      const float4 y = pre[(0 * SR + s) * NT + threadIdx.x];
+      const long long g = g0 + (long long)s * a.nx;
+      const float4 y = PF ? pre[(0 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.x + g);
       float2 y0 = lo2(y), y1 = hi2(y);
       if (a.beta != 0.f) {
-        const float4 o = pre[(1 * SR + s) * NT + threadIdx.x];
+        const float4 o = PF ? pre[(1 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.xp + g);
         y0 = fma2(cb, y0, mul2(cm, lo2(o)));
         y1 = fma2(cb, y1, mul2(cm, hi2(o)));
       }
       if (a.grad) {
-        float4 gg = pre[(2 * SR + s) * NT + threadIdx.x];
+        float4 gg = PF ? pre[(2 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.grad + g);
         if (a.real_mode) gg.y = gg.w = 0.f;  // real engine: Re(grad) only
         y0 = fma2(cs, lo2(gg), y0);
         y1 = fma2(cs, hi2(gg), y1);
@@ -151,7 +161,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
     // the slots are free again (each thread only reads its own): overlap the
     // next region's HBM reads with this region's FGP iterations
-    if (next_work >= 0) prefetch_tile(a, pre_next, next_work);
+    if (PF && next_work >= 0) prefetch_tile(a, pre_next, next_work);
   }
 
   // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
@@ -163,13 +173,15 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   // of column 0 is lane-1's column 1 (own value at the region's left edge)
   auto gx_row = [&](float2 x0, float2 x1, float2& gx0, float2& gx1) {
     const float2 l = shfl_up(x1);
-    gx0 = lane0 ? make_float2(0.f, 0.f) : sub2(x0, l);
+    gx0 = sub2(x0, l);
+    if (EDGE && lane0) gx0 = make_float2(0.f, 0.f);
     gx1 = sub2(x1, x0);
   };
   // right neighbour of column 1 = lane+1's column 0 (0 beyond the region)
   auto right_of = [&](float2 x0) {
-    const float2 r = shfl_dn(x0);
-    return lane31 ? make_float2(0.f, 0.f) : r;
+    float2 r = shfl_dn(x0);
+    if (EDGE && lane31) r = make_float2(0.f, 0.f);
+    return r;
   };
   auto above_of = [&](int k, float2 self) -> float2 {
     if (w == 0) return self;  // region top row: zero y-difference
@@ -349,15 +361,15 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       const uint32_t rowbits = (mInt >> (2 * s)) & 3u;
       if (!rowbits) continue;
       const long long g = g0 + (long long)s * a.nx;
-      const float4 y4 = pre[(0 * SR + s) * NT + threadIdx.x];
+      const float4 y4 = PF ? pre[(0 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.x + g);
       float2 y[2] = {lo2(y4), hi2(y4)};
       if (a.beta != 0.f) {
-        const float4 o = pre[(1 * SR + s) * NT + threadIdx.x];
+        const float4 o = PF ? pre[(1 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.xp + g);
         y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
         y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
       }
       float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.grad) gr4 = pre[(2 * SR + s) * NT + threadIdx.x];
+      if (a.grad) gr4 = PF ? pre[(2 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.grad + g);
       if (a.real_mode) gr4.y = gr4.w = 0.f;
       const float2 gr[2] = {lo2(gr4), hi2(gr4)};
 #pragma unroll
@@ -379,19 +391,33 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       }
     }
   }
-  double accd[kProxParts];
+  // fp32 warp sums (32 terms each), then fp64 across the 16 warps
+  __shared__ float wsum[NW][kProxParts];
 #pragma unroll
-  for (int i = 0; i < kProxParts; ++i) accd[i] = (double)acc[i];
-  block_sum<kProxParts, NT>(accd, a.part + ((long long)plane * a.tiles_per_plane + tile) * kProxParts);
-  __syncthreads();  // band buffers are reused by the next region
+  for (int i = 0; i < kProxParts; ++i) {
+    float x = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) wsum[w][i] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < kProxParts) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t += (double)wsum[k][threadIdx.x];
+    a.part[((long long)plane * a.tiles_per_plane + tile) * kProxParts + threadIdx.x] = t;
+  }
+  __syncthreads();  // band buffers and wsum are reused by the next region
 }
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
 template <bool TV>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
-  __shared__ Bands sm;
-  extern __shared__ float4 pre[];  // [2][3][SR][NT] double-buffered prefetch slots
+  static_assert(NT <= 1024, "");
+  extern __shared__ float4 dyn[];  // Bands, then (PF) [2][3][SR][NT] double-buffered prefetch slots
+  Bands& sm = *reinterpret_cast<Bands*>(dyn);
+  float4* pre = dyn + sizeof(Bands) / sizeof(float4);
   const int total = a.tiles_per_plane * a.nplanes;
   auto next_from = [&](int t) {
     if (a.force)
@@ -400,10 +426,15 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   };
   int work = next_from(blockIdx.x);
   if (work < 0) return;
-  prefetch_tile(a, pre, work);
+  if (PF) prefetch_tile(a, pre, work);
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nxt = next_from(work + gridDim.x);
-    prox_tile<TV>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+    const TileGeom tg = tile_geom(a, work % a.tiles_per_plane);
+    const bool edge = tg.rj0 == 0 || tg.rj0 + RW == a.nx;
+    if (edge)
+      prox_tile<TV, true>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+    else
+      prox_tile<TV, false>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
     work = nxt;
   }
 }
@@ -442,7 +473,7 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(float4) * 2 * 3 * SR * NT;
+  const size_t smem = sizeof(Bands) + (PF ? sizeof(float4) * 2 * 3 * SR * NT : 0);
   const long long total = (long long)a.tiles_per_plane * a.nplanes;
   const int grid = (int)std::min<long long>(total, nsm);
   if (grid <= 0) return cudaSuccess;
