@@ -35,7 +35,7 @@ CONFIGS = {
     "c1": (256, 256, 64, 50, None, 0, 0.5, 0.2, 5, 20e-6),
     "c2": (1024, 1024, 256, 100, 0.05, 1, 0.5, 0.2, 5, 20e-6),
     "c3": (1024, 1024, 512, 100, 0.2, 2, 0.5, 0.2, 5, 20e-6),
-    "c5": (1024, 1024, 512, 100, 0.05, 4, 0.05, 1.0, 20, 20e-6),
+    "c5": (1024, 1024, 512, 100, 0.05, 4, 0.05, 1.0, 20, 20e-6),  # rods (microfibers), length 10 d
 }
 METRIC = "voxel-iterations/sec (1024²×512 fused-lasso FISTA) at 1/2/4/8 B200; % HBM roofline"
 BYTES_PER_VOXEL_ITER = 72  # SURVEY.md 8(d) algorithmic bytes per voxel-iteration
@@ -44,44 +44,28 @@ KERNEL_BYTES = {"prox": 32, "adj_cols": 8, "adj_rows": 16, "fwd_rows": 16, "fwd_
 
 
 def n_particles(cfg):
-    nx, _, _, _, sd, _, _, _, _, d = cfg
+    nx, _, _, _, sd, _, _, _, inner, d = cfg
     if sd is None:
         return 50
-    return int(round(sd * (nx * PITCH) ** 2 / d ** 2))
+    area = d ** 2 if cfg is not CONFIGS.get("c5") else 7.9 * d ** 2  # mean projected rod area ~ pi/4 * 10 d^2
+    return int(round(sd * (nx * PITCH) ** 2 / area))
 
 
-def render_gpu(points, nx, ny, diameter, device, batch=32):
-    """|1 - ifft2(sum_p fft2(disk_p) H(-z_p))|^2 (synth.py:161-181), float64 on the
-    GPU.  Benchmark-input generation only (not timed, not the hot path)."""
-    import torch
-    fy = torch.fft.fftfreq(ny, d=PITCH, dtype=torch.float64, device=device)[:, None]
-    fx = torch.fft.fftfreq(nx, d=PITCH, dtype=torch.float64, device=device)[None, :]
-    arg = 1.0 - (LAM * fx) ** 2 - (LAM * fy) ** 2
-    keep = arg >= 0
-    root = torch.sqrt(torch.clamp(arg, min=0.0))
-    xs = torch.arange(nx, dtype=torch.float64, device=device) * PITCH
-    ys = torch.arange(ny, dtype=torch.float64, device=device) * PITCH
-    spec = torch.zeros((ny, nx), dtype=torch.complex128, device=device)
-    pts = torch.as_tensor(points, dtype=torch.float64, device=device)
-    r2 = (diameter / 2.0) ** 2
-    for s in range(0, len(pts), batch):
-        p = pts[s:s + batch]
-        disk = ((xs[None, None, :] - p[:, 0, None, None]) ** 2 + (ys[None, :, None] - p[:, 1, None, None]) ** 2) <= r2
-        f = torch.fft.fft2(disk.to(torch.float64))
-        ph = (-2.0 * math.pi / LAM) * p[:, 2, None, None] * root[None]
-        spec += (f * torch.polar(keep.to(torch.float64).expand_as(ph), ph)).sum(0)
-    fld = torch.fft.ifft2(spec)
-    return (torch.abs(1.0 - fld) ** 2).cpu().numpy()
-
-
-def make_hologram(cfg, device):
-    from oracle.holo_oracle import Geometry, add_noise, invert_residual, make_scene
+def make_hologram(cfg, device=None):
+    """Synthetic C-config hologram: seeded scene, GPU render (holo_render_spectrum +
+    library FFT, fp64 accumulation), noise sigma 0.02, b = 1 - I/mean(I)
+    (synth.py:74-191, preprocess.py:41-53).  Input generation, not timed."""
+    from paper_1904_04884_b200 import VolumeGeometry
+    from paper_1904_04884_b200.synth import add_noise, generate_scene, invert_residual, render_hologram
     nx, ny, nz, _, _, seed, *_rest = cfg
-    d = cfg[9]
-    g = Geometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
-    pts = make_scene(n_particles(cfg), g, d, seed=seed, margin_planes=2)
-    img = render_gpu(pts, nx, ny, d, device)
-    return invert_residual(add_noise(img, 0.02, seed=seed + 7))
+    g = VolumeGeometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
+    sc = generate_scene(n_particles(cfg), g, cfg[9], seed=seed, margin_planes=2)
+    if cfg is CONFIGS["c5"]:  # microfibers: random unit orientation, length 10 d (SURVEY 8d C5)
+        rng = np.random.default_rng(seed + 100)
+        for p in sc.particles:
+            o = rng.standard_normal(3)
+            p.orientation, p.length = o / np.linalg.norm(o), 10 * cfg[9]
+    return invert_residual(add_noise(render_hologram(sc), 0.02, seed=seed + 7))
 
 
 class ClockSampler:

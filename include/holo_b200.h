@@ -104,10 +104,12 @@ int holo_solve_device(holo_handle* h, const double* b_dev, const holo_solver_con
 int holo_history(const holo_handle* h, double* out, int32_t cap, int32_t* n);
 
 /* sparsevol.py:75-88 from_dense over the solution: nnz per local plane, then
- * COO entries sorted by (plane, row, col); vals are complex64 pairs.
- * _host copies into host buffers, _device fills device buffers. */
+ * COO entries sorted by (plane, row, col).  _host fills host arrays with
+ * complex128 values (re, im doubles; the reference's SparsePlane.values
+ * dtype), widened on the device; _device fills device buffers with
+ * complex64 pairs. */
 int holo_plane_nnz(holo_handle* h, int64_t* nnz_per_local_plane);
-int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz);
+int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, double* vals, int64_t cap, int64_t* nnz);
 int holo_export_coo_device(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz,
                            void* stream);
 /* device pointer to the dense complex64 solution (local planes) */
@@ -129,6 +131,29 @@ int holo_op_adjoint(holo_handle* h, const void* r, void* out, double scale, void
  * including the per-plane guard (prox.py:138-147). */
 int holo_op_prox_fl(holo_handle* h, const void* v, void* out, int32_t nplanes, int32_t ny, int32_t nx, double tau_l1,
                     double tau_tv, int32_t inner, void* stream);
+
+/* ---- output side ---- */
+/* segment.py:106-146 connected_components, 26-connectivity, on the GPU.
+ * kij: n voxel coordinates (k, i, j) int32, sorted lexicographically (the COO
+ * export order), device memory.  roots[u] (device) = smallest voxel id of
+ * u's component, so components ordered by root are in the reference's
+ * emission order (sorted by smallest voxel). */
+int holo_label_components(const int32_t* kij, int64_t n, int32_t nz, int32_t ny, int32_t nx, int32_t* roots,
+                          void* stream);
+
+/* ---- input side ---- */
+/* synth.py:161-181 render_hologram's spectrum: spec[f] = sum_p fft2(mask_p)(f) *
+ * exp(-i 2 pi z_p/lam sqrt(1 - (lam f)^2)) (0 where evanescent), particles in
+ * order.  Particle p owns mask pixels pix_yx[2e..2e+1] (row, col) with
+ * amplitudes pix_a[e] for e in [pix_off[p], pix_off[p+1]).  All device
+ * pointers; spec is complex128 (ny*nx).  fp64 throughout, like the reference. */
+int holo_render_spectrum(const double* z_over_lam, const int32_t* pix_off, const int32_t* pix_yx, const double* pix_a,
+                         int32_t n, int32_t ny, int32_t nx, double pitch, double wavelength, void* spec, void* stream);
+/* preprocess.py:17-38: out[t] = (I_t - M_t) / sqrt(max(M_t, 1e-12)), M_t the mean of
+ * frames [t-w/2, t+w/2] (truncated at the ends) excluding frame t; fp64 device
+ * stacks (T, ny, nx); window odd, 3 <= window <= T. */
+int holo_background(const double* images, int32_t T, int32_t ny, int32_t nx, int32_t window, double* out,
+                    void* stream);
 
 /* ---- instrumentation ---- */
 /* per-kernel-class device time (CUDA events on the launching stream) */

@@ -76,6 +76,9 @@ SIGNATURES = {
     "holo_op_forward": (ctypes.c_int, [_H, _P, _P, _P]),
     "holo_op_adjoint": (ctypes.c_int, [_H, _P, _P, _D, _P]),
     "holo_op_prox_fl": (ctypes.c_int, [_H, _P, _P, _I, _I, _I, _D, _D, _I, _P]),
+    "holo_label_components": (ctypes.c_int, [_P, ctypes.c_int64, _I, _I, _I, _P, _P]),
+    "holo_render_spectrum": (ctypes.c_int, [_P, _P, _P, _P, _I, _I, _I, _D, _D, _P, _P]),
+    "holo_background": (ctypes.c_int, [_P, _I, _I, _I, _I, _P, _P]),
     "holo_profile_enable": (ctypes.c_int, [_H, _I]),
     "holo_profile_read": (ctypes.c_int, [_H, ctypes.POINTER(_I), _P, _P, _P]),
     "holo_launch_count": (ctypes.c_int64, []),

@@ -206,6 +206,11 @@ struct Engine {
   long long* coo_offsets = nullptr;
   std::vector<int> h_counts;
   std::vector<long long> h_offsets;
+  // device staging for host exports (grow-only)
+  int32_t* coo_rows = nullptr;
+  int32_t* coo_cols = nullptr;
+  double2* coo_vals = nullptr;
+  long long coo_cap = 0;
   double real_sigma2 = -1.0;  // cached ||A_real||^2
   // results of the last solve
   int ix = 0;  // slot holding the solution
@@ -223,6 +228,7 @@ struct Engine {
     cudaFree(sens_part); cudaFree(scal); cudaFreeHost(h_scal); cudaFree(prox_part);
     cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(fgp_beta);
     cudaFree(coo_counts); cudaFree(coo_offsets);
+    cudaFree(coo_rows); cudaFree(coo_cols); cudaFree(coo_vals);
     plan_free(plan);
 #ifdef HOLO_WITH_NCCL
     if (comm) ncclCommDestroy(comm);
@@ -402,6 +408,8 @@ struct Engine {
     int rc = ensure_volume();
     if (rc) return rc;
     const long long n = (long long)nzl * P;
+    counted_slot = -1;
+    have_solution = false;
     if (n) HOLO_CUDA(cudaMemcpyAsync(X[0], v0, sizeof(float2) * n, cudaMemcpyDeviceToDevice, s));
     float2* v = X[0];
     if (real) HOLO_CUDA(vol_rescale(v, n, nullptr, 1, s));
@@ -503,8 +511,20 @@ struct Engine {
     }
   }
 
+  int counted_slot = -1;  // slot whose chunk counts/offsets are current (host + device)
+  long long counted_total = 0;
+
   int count_nnz(int slot, long long& total, std::vector<long long>* per_plane, cudaStream_t s) {
     const int nch = coo_chunks(P, std::max(nzl, 1));
+    if (slot == counted_slot && nzl > 0) {  // the solution has not changed since the last count
+      total = counted_total;
+      if (per_plane) {
+        const int cpp = nch / nzl;
+        per_plane->assign(nzl, 0);
+        for (int i = 0; i < nch; ++i) (*per_plane)[i / cpp] += h_counts[i];
+      }
+      return HOLO_OK;
+    }
     HOLO_CUDA(dalloc(coo_counts, nch));
     HOLO_CUDA(dalloc(coo_offsets, nch));
     h_counts.resize(nch);
@@ -527,6 +547,8 @@ struct Engine {
     }
     total = run;
     HOLO_CUDA(cudaMemcpyAsync(coo_offsets, h_offsets.data(), sizeof(long long) * nch, cudaMemcpyHostToDevice, s));
+    counted_slot = slot;
+    counted_total = run;
     return HOLO_OK;
   }
 
@@ -545,6 +567,7 @@ struct Engine {
     last = holo_report{};
     history.clear();
     have_solution = false;
+    counted_slot = -1;
     const size_t vbytes = sizeof(float2) * (size_t)nzl * P;
     for (int i = 0; i < 3; ++i) {
       if (vbytes) HOLO_CUDA(cudaMemsetAsync(X[i], 0, vbytes, s));
@@ -792,8 +815,8 @@ int holo_plane_nnz(holo_handle* h, int64_t* nnz_per_local_plane) {
   })
 }
 
-static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz,
-                      bool host, cudaStream_t s) {
+static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, void* vals, int64_t cap, int64_t* nnz, bool host,
+                      cudaStream_t s) {
   Engine& e = h->e;
   if (!e.have_solution) return fail(HOLO_ERR_INVALID, "no solution: call holo_solve first");
   long long tot = 0;
@@ -802,27 +825,33 @@ static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, float* vals,
   if (nnz) *nnz = tot;
   if (tot > cap) return fail(HOLO_ERR_INVALID, "COO capacity too small");
   if (tot == 0) return HOLO_OK;
-  int32_t *dr = rows, *dc = cols;
-  float2* dv = (float2*)vals;
-  if (host) {
-    HOLO_CUDA(cudaMalloc(&dr, sizeof(int32_t) * tot));
-    HOLO_CUDA(cudaMalloc(&dc, sizeof(int32_t) * tot));
-    HOLO_CUDA(cudaMalloc(&dv, sizeof(float2) * tot));
+  if (!host) {
+    HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, rows, cols, (float2*)vals, nullptr, s));
+    return HOLO_OK;
   }
-  HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, dr, dc, dv, s));
-  if (host) {
-    HOLO_CUDA(cudaMemcpyAsync(rows, dr, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
-    HOLO_CUDA(cudaMemcpyAsync(cols, dc, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
-    HOLO_CUDA(cudaMemcpyAsync(vals, dv, sizeof(float2) * tot, cudaMemcpyDeviceToHost, s));
-    HOLO_CUDA(cudaStreamSynchronize(s));
-    cudaFree(dr);
-    cudaFree(dc);
-    cudaFree(dv);
+  if (tot > e.coo_cap) {  // grow-only device staging, reused across exports
+    cudaFree(e.coo_rows);
+    cudaFree(e.coo_cols);
+    cudaFree(e.coo_vals);
+    e.coo_rows = e.coo_cols = nullptr;
+    e.coo_vals = nullptr;
+    const long long cap2 = tot + tot / 4;
+    HOLO_CUDA(cudaMalloc(&e.coo_rows, sizeof(int32_t) * cap2));
+    HOLO_CUDA(cudaMalloc(&e.coo_cols, sizeof(int32_t) * cap2));
+    HOLO_CUDA(cudaMalloc(&e.coo_vals, sizeof(double2) * cap2));
+    e.coo_cap = cap2;
   }
+  // values widened to complex128 on the device: the caller's arrays are final
+  HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, e.coo_rows, e.coo_cols, nullptr,
+                              e.coo_vals, s));
+  HOLO_CUDA(cudaMemcpyAsync(rows, e.coo_rows, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
+  HOLO_CUDA(cudaMemcpyAsync(cols, e.coo_cols, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
+  HOLO_CUDA(cudaMemcpyAsync(vals, e.coo_vals, sizeof(double2) * tot, cudaMemcpyDeviceToHost, s));
+  HOLO_CUDA(cudaStreamSynchronize(s));
   return HOLO_OK;
 }
 
-int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, float* vals, int64_t cap, int64_t* nnz) {
+int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, double* vals, int64_t cap, int64_t* nnz) {
   GUARD_HANDLE(h);
   TRY({ return export_coo(h, rows, cols, vals, cap, nnz, true, h->e.stream); })
 }

@@ -47,8 +47,8 @@ struct TwLayout {
     return off;
   }
   static constexpr int size() {
-    int off = 0;
     if (N <= 16) return 1;
+    int off = 0;
     for (int s = 16; s < N; s *= radix(s)) off += (radix(s) - 1) * s;
     return off;
   }
@@ -209,7 +209,6 @@ HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const f
     for (int r = 0; r < R; ++r) a[r] = v[s + r * BPT];
     if constexpr (NS > 1) {
       const int kk = b % NS;
-#pragma unroll
       const float4* tp = tw + TwLayout<N>::offset(NS) + kk;
       // groups of 4 twiddles: bounds the 4-register table entries in flight
 #pragma unroll

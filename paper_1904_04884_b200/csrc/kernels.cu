@@ -695,11 +695,12 @@ __global__ void __launch_bounds__(kCooThreads) k_coo_count(const float2* __restr
   if (threadIdx.x == 0) counts[(long long)plane * cpp + ch] = (int)res[0];
 }
 
-// row-major compaction: each thread owns 4 consecutive elements of the chunk
+// row-major compaction: each thread owns 4 consecutive elements of the chunk;
+// values are written as complex64 (vals) or widened to complex128 (vals64)
 __global__ void __launch_bounds__(kCooThreads) k_coo_compact(const float2* __restrict__ x, long long P, int nx,
                                                              int cpp, const long long* __restrict__ offsets,
                                                              int* __restrict__ rows, int* __restrict__ cols,
-                                                             float2* __restrict__ vals) {
+                                                             float2* __restrict__ vals, double2* __restrict__ vals64) {
   constexpr int PER = kCooChunk / kCooThreads;
   const int plane = blockIdx.y, ch = blockIdx.x;
   const long long start = (long long)ch * kCooChunk + (long long)threadIdx.x * PER;
@@ -733,7 +734,10 @@ __global__ void __launch_bounds__(kCooThreads) k_coo_compact(const float2* __res
       const long long p = start + e;
       rows[out] = (int)(p / nx);
       cols[out] = (int)(p % nx);
-      vals[out] = v[e];
+      if (vals64)
+        vals64[out] = make_double2((double)v[e].x, (double)v[e].y);
+      else
+        vals[out] = v[e];
       ++out;
     }
   }
@@ -1055,9 +1059,9 @@ cudaError_t coo_count(const float2* x, long long P, int nplanes, int* chunk_coun
 }
 
 cudaError_t coo_compact(const float2* x, long long P, int nx, int nplanes, const long long* chunk_offsets, int* rows,
-                        int* cols, float2* vals, cudaStream_t s) {
+                        int* cols, float2* vals, double2* vals64, cudaStream_t s) {
   const int cpp = (int)((P + kCooChunk - 1) / kCooChunk);
-  k_coo_compact<<<dim3(cpp, nplanes), kCooThreads, 0, s>>>(x, P, nx, cpp, chunk_offsets, rows, cols, vals);
+  k_coo_compact<<<dim3(cpp, nplanes), kCooThreads, 0, s>>>(x, P, nx, cpp, chunk_offsets, rows, cols, vals, vals64);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

@@ -110,6 +110,6 @@ cudaError_t vol_rescale(float2* x, long long n, const double* nrm2, int real, cu
 int coo_chunks(long long P, int nplanes);
 cudaError_t coo_count(const float2* x, long long P, int nplanes, int* chunk_counts, cudaStream_t s);
 cudaError_t coo_compact(const float2* x, long long P, int nx, int nplanes, const long long* chunk_offsets,
-                        int* rows, int* cols, float2* vals, cudaStream_t s);
+                        int* rows, int* cols, float2* vals, double2* vals64, cudaStream_t s);
 
 }  // namespace holo

@@ -113,18 +113,19 @@ class HoloEngine:
         return out[: self.nz_local]
 
     def export_coo(self):
-        """(plane_nnz, rows, cols, values complex128) of the local planes."""
+        """(plane_nnz, rows int32, cols int32, values complex128) of the local planes,
+        written by the device straight into the returned arrays."""
         per = self.plane_nnz()
         tot = int(per.sum())
-        rows = np.zeros(max(tot, 1), np.int32)
-        cols = np.zeros(max(tot, 1), np.int32)
-        vals = np.zeros(max(tot, 1), np.complex64)
+        rows = np.empty(max(tot, 1), np.int32)
+        cols = np.empty(max(tot, 1), np.int32)
+        vals = np.empty(max(tot, 1), np.complex128)
         n = ctypes.c_int64()
         nat.check(self.lib.holo_export_coo_host(self.h, rows.ctypes.data_as(ctypes.c_void_p),
                                                 cols.ctypes.data_as(ctypes.c_void_p),
                                                 vals.ctypes.data_as(ctypes.c_void_p), tot, ctypes.byref(n)))
         assert n.value == tot
-        return per, rows[:tot], cols[:tot], vals[:tot].astype(np.complex128)
+        return per, rows[:tot], cols[:tot], vals[:tot]
 
     def solution_dense(self):
         """Dense complex64 solution of the local planes as a CUDA tensor (device copy)."""

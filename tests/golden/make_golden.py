@@ -174,6 +174,77 @@ def main():
              gradient=np.concatenate([gc for _, _, gc in eng.gradient_chunks(r, 4)]),
              sigma2=np.array(solver.estimate_operator_norm(gr, real=True)),
              sigma2_g64=np.array(solver.estimate_operator_norm(g64, real=True)))
+    if want("render"):
+        # input side: nonlinear renders (disks, rods, a sub-pixel particle) and background removal
+        g = VolumeGeometry(64, 32, 16, PITCH, DZ, Z0, LAM)
+        sc = synth.generate_scene(12, g, 20e-6, seed=21, margin_planes=2)
+        img_disk = synth.render_hologram(sc)
+        rng = np.random.default_rng(22)
+        rods = []
+        for _ in range(5):
+            o = rng.standard_normal(3)
+            o /= np.linalg.norm(o)
+            rods.append(synth.Particle(x=rng.uniform(0, g.nx * g.pitch), y=rng.uniform(0, g.ny * g.pitch),
+                                       z=rng.uniform(g.z0, g.z0 + g.nz * g.dz), diameter=20e-6,
+                                       orientation=o, length=200e-6, opacity=0.8))
+        rods.append(synth.Particle(x=101e-6, y=203e-6, z=g.z0 + 3e-5, diameter=5e-6))
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            img_rod = synth.render_hologram(synth.Scene(rods, g))
+        rod_arr = np.array([[p.x, p.y, p.z, p.diameter, p.opacity,
+                             *(p.orientation if p.orientation is not None else [np.nan] * 3),
+                             p.length if p.length is not None else np.nan] for p in rods])
+        stack = rng.random((9, 8, 10)) + 0.5
+        from holotrack.preprocess import preprocess_background
+        save("render", geom=geom_arr(g), scene=sc.positions(), img_disk=img_disk, rods=rod_arr, img_rod=img_rod,
+             noisy=synth.add_noise(img_disk, 0.02, seed=5), stack=stack, background=preprocess_background(stack, 5))
+    if want("pipeline"):
+        # the reference CLI end to end: 2 frames, invert residuals, step once, fista, segment, tables
+        import tempfile
+        from holotrack import cli as hcli
+        import yaml
+        g = VolumeGeometry(64, 64, 16, PITCH, DZ, Z0, LAM)
+        cfgd = {"geometry": dict(nx=64, ny=64, nz=16, pitch=PITCH, dz=DZ, z0=Z0, wavelength=LAM),
+                "solver": dict(max_iters=15), "segmentation": dict(min_vox=2, with_orientation=True),
+                "preprocessing": dict(mode="invert")}
+        with tempfile.TemporaryDirectory() as td:
+            frames = []
+            for t in range(2):
+                sc = synth.generate_scene(6, g, 20e-6, seed=30 + t, margin_planes=2)
+                img = synth.add_noise(synth.render_hologram(sc), 0.02, seed=40 + t)
+                frames.append(img.astype("<f4"))
+                from holotrack import io as hio
+                hio.save_image(os.path.join(td, f"hologram_{t:04d}.f32"), img)
+            cpath = os.path.join(td, "cfg.yaml")
+            cfgd["paths"] = dict(output=td)
+            with open(cpath, "w") as f:
+                yaml.safe_dump(cfgd, f)
+            assert hcli.main(["reconstruct", "--config", cpath]) == 0
+            parts = open(os.path.join(td, "particles.tsv")).read()
+            objs = [open(os.path.join(td, f"objective_{t:04d}.tsv")).read() for t in range(2)]
+            vols = [np.frombuffer(open(os.path.join(td, f"volume_{t:04d}.rihv"), "rb").read(), np.uint8)
+                    for t in range(2)]
+        save("pipeline", frames=np.stack(frames), config=np.array(yaml.safe_dump(cfgd)), particles=np.array(parts),
+             objective0=np.array(objs[0]), objective1=np.array(objs[1]), rihv0=vols[0], rihv1=vols[1])
+    if want("segment"):
+        # output side: RIHV container bytes and detections with orientation
+        d = np.load(os.path.join(HERE, "fista_128.npz"))
+        g = VolumeGeometry(*[int(x) for x in d["geom"][:3]], *d["geom"][3:])
+        dense = np.zeros((g.nz, g.ny, g.nx), dtype=np.complex128)
+        dense[d["k"], d["r"], d["c"]] = d["v"]
+        vol = sparsevol.SparseVolume.from_dense_stack(dense, g)
+        dets = segment.extract_particles(vol, 2 / 256, 2, with_orientation=True)
+        rows = []
+        for det in dets:
+            ax = det.axis if det.axis is not None else np.full(3, np.nan)
+            el = det.elongation if det.elongation is not None else np.nan
+            rows.append([det.blob_id, det.x_vox, det.y_vox, det.z_vox, det.x, det.y, det.z, det.volume,
+                         det.peak_intensity, *ax, el])
+        path = os.path.join("/tmp", "golden_128.rihv")
+        sparsevol.save_volume(path, vol)
+        blob = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+        save("segment", dets=np.array(rows), rihv=blob, rel_tol=np.array(2 / 256), min_vox=np.array(2))
     if want("c1") and not a.skip_c1:
         gc1 = VolumeGeometry(256, 256, 64, PITCH, DZ, Z0, LAM)
         bc1, tc1 = hologram(gc1, 50, 20e-6, 0)
