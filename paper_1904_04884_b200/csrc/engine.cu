@@ -201,6 +201,12 @@ struct Engine {
   uint8_t* force_acc = nullptr; // [nzl]
   float* fgp_beta = nullptr;
   int fgp_cap = 0;
+  // multi-pass FGP state (large T): v, 2 halves of (p,q) and (rp,rq), per-tile TV(v)
+  float2* mp_v = nullptr;
+  float4* mp_s = nullptr;
+  float4* mp_r = nullptr;
+  float* mp_tvv = nullptr;
+  long long mp_cap = 0, mp_tiles = 0;
   // coo
   int* coo_counts = nullptr;
   long long* coo_offsets = nullptr;
@@ -229,6 +235,7 @@ struct Engine {
     cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(fgp_beta);
     cudaFree(coo_counts); cudaFree(coo_offsets);
     cudaFree(coo_rows); cudaFree(coo_cols); cudaFree(coo_vals);
+    cudaFree(mp_v); cudaFree(mp_s); cudaFree(mp_r); cudaFree(mp_tvv);
     plan_free(plan);
 #ifdef HOLO_WITH_NCCL
     if (comm) ncclCommDestroy(comm);
@@ -303,6 +310,29 @@ struct Engine {
       prox_part_cap = need;
     }
     a.part = prox_part;
+    if (a.pass_len) {  // multi-pass FGP state
+      const long long n = (long long)std::max(nplanes, 1) * ny * nx;
+      const long long tiles = (long long)std::max(nplanes, 1) * a.tiles_per_plane;
+      if (n > mp_cap) {
+        cudaFree(mp_v); cudaFree(mp_s); cudaFree(mp_r);
+        mp_v = nullptr; mp_s = nullptr; mp_r = nullptr;
+        HOLO_CUDA(cudaMalloc(&mp_v, sizeof(float2) * n));
+        HOLO_CUDA(cudaMalloc(&mp_s, sizeof(float4) * 2 * n));
+        HOLO_CUDA(cudaMalloc(&mp_r, sizeof(float4) * 2 * n));
+        mp_cap = n;
+      }
+      if (tiles > mp_tiles) {
+        cudaFree(mp_tvv);
+        mp_tvv = nullptr;
+        HOLO_CUDA(cudaMalloc(&mp_tvv, sizeof(float) * 2 * tiles));
+        mp_tiles = tiles;
+      }
+      a.vbuf = mp_v;
+      a.sbuf = mp_s;
+      a.rbuf = mp_r;
+      a.sstride = n;
+      a.tvv = mp_tvv;
+    }
     if (inner > fgp_cap) {
       cudaFree(fgp_beta);
       fgp_beta = nullptr;

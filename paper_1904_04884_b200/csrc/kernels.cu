@@ -952,8 +952,22 @@ bool prox_supported(int ny, int nx, int inner) {
 
 cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
   if (a.kind == 1) {
-    COUNT_LAUNCH(1);
-    return prox_strip(a, s);
+    if (!a.pass_len) {
+      COUNT_LAUNCH(1);
+      return prox_strip(a, s);
+    }
+    if (!a.vbuf || !a.sbuf || !a.rbuf || !a.tvv) return cudaErrorInvalidValue;
+    // guard fix-up (force): the state of every pass is still in HBM, rerun the last
+    const int last0 = ((a.inner - 1) / a.pass_len) * a.pass_len;
+    for (int t0 = a.force ? last0 : 0; t0 < a.inner; t0 += a.pass_len) {
+      ProxArgs b = a;
+      b.t0 = t0;
+      b.t1 = std::min(a.inner, t0 + a.pass_len);
+      COUNT_LAUNCH(1);
+      cudaError_t e = prox_strip(b, s);
+      if (e) return e;
+    }
+    return cudaSuccess;
   }
   const int ew = std::min(a.nx, a.tile + 2 * a.halo), eh = std::min(a.ny, a.tile + 2 * a.halo);
   if (ew * eh > kProxThreads * kProxMaxPx) return cudaErrorInvalidValue;

@@ -39,6 +39,15 @@ struct ProxArgs {
   float fgpb[16] = {};              // same schedule by value (strip kernel, inner <= 12)
   const uint8_t* force = nullptr;   // guard fix-up pass: per plane bit0 re / bit1 im -> identity
   double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts]
+  // multi-pass FGP (strip kernel, large T): this launch runs iterations [t0, t1);
+  // the dual state crosses launches through HBM (interior pixels written,
+  // region + halo read back by the next pass)
+  int t0 = 0, t1 = 0, pass_len = 0;  // pass_len 0: single pass
+  float2* vbuf = nullptr;            // v = y - step grad (first pass writes)
+  float4* sbuf = nullptr;            // (p, q) per pixel, two halves (pass parity)
+  float4* rbuf = nullptr;            // extrapolated (rp, rq) per pixel, two halves
+  long long sstride = 0;             // elements per half: pass i writes half i&1, reads (i-1)&1
+  float* tvv = nullptr;              // per-tile TV(v) partials [tile][2], first pass -> last pass
 };
 
 bool plan_supported(int nx, int ny);
@@ -73,6 +82,7 @@ bool prox_supported(int ny, int nx, int inner);
 // register-strip prox (prox_strip.cu): used when the halo T+2 <= prox_strip_max_halo()
 int prox_strip_max_halo();
 bool prox_strip_applicable(int ny, int nx, int inner);
+int prox_strip_pass_len(int inner);  // 0: single pass; else FGP iterations per pass
 void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner);
 cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s);
 cudaError_t prox(const ProxArgs& a, cudaStream_t s);

@@ -137,7 +137,29 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   const long long g0 = strip_base(a, plane, tg);
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
-  {
+  const bool first = a.t0 == 0, last = a.t1 >= a.inner;
+  const int pass = a.pass_len ? a.t0 / a.pass_len : 0;
+  // state halves alternate by pass parity so a pass never overwrites what
+  // neighbouring regions of the same launch still read as their halo
+  const float4* s_in = a.sbuf + ((pass - 1) & 1) * a.sstride;
+  const float4* r_in = a.rbuf + ((pass - 1) & 1) * a.sstride;
+  if (!first) {  // later pass of a multi-pass FGP: v and the dual state from HBM
+#pragma unroll
+    for (int s = 0; s < SR; ++s) {
+      const long long g = g0 + (long long)s * a.nx;
+      const float4 vv = *reinterpret_cast<const float4*>(a.vbuf + g);
+      v[s][0] = lo2(vv);
+      v[s][1] = hi2(vv);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float4 sq = s_in[g + k], rr = r_in[g + k];
+        p[s][k] = lo2(sq);
+        q[s][k] = hi2(sq);
+        rp[s][k] = lo2(rr);
+        rq[s][k] = hi2(rr);
+      }
+    }
+  } else {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
     if (PF) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // my slots for this tile have landed
 #pragma unroll
@@ -161,7 +183,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
     // the slots are free again (each thread only reads its own): overlap the
     // next region's HBM reads with this region's FGP iterations
-    if (PF && next_work >= 0) prefetch_tile(a, pre_next, next_work);
+    if (PF && next_work >= 0) prefetch_tile(a, pre_next, next_work);  // (first pass only)
   }
 
   // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
@@ -192,6 +214,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
 
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
+    if (first) {
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
     sm.bot[w][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     __syncthreads();
@@ -226,8 +249,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
     sm.top[0][w][lane] = f4(rp[0][0], rp[0][1]);
     __syncthreads();
-    // ---- iterations 1..T-1: one fused sweep down the band per iteration ----
-    for (int t = 1; t < a.inner; ++t) {
+    } else {
+      sm.top[(a.t0 - 1) & 1][w][lane] = f4(rp[0][0], rp[0][1]);  // the buffer the first sweep reads
+      __syncthreads();
+    }
+    // ---- iterations max(t0,1)..t1-1: one fused sweep down the band per iteration ----
+    for (int t = first ? 1 : a.t0; t < a.t1; ++t) {
       const int b = (t - 1) & 1;  // buffer holding this iteration's band-top rp
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
       // u(s, k) = v - tau (rp + rq - rp_down - rq_right)
@@ -278,6 +305,42 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       }
       sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffer: slower warps may read b
       __syncthreads();
+    }
+    if (!last) {
+      // hand the dual state (and v, once) of the interior pixels to the next pass
+#pragma unroll
+      for (int s = 0; s < SR; ++s) {
+        const long long g = g0 + (long long)s * a.nx;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!(mInt & (1u << (2 * s + k)))) continue;
+          a.sbuf[(pass & 1) * a.sstride + g + k] = f4(p[s][k], q[s][k]);
+          a.rbuf[(pass & 1) * a.sstride + g + k] = f4(rp[s][k], rq[s][k]);
+          if (first) a.vbuf[g + k] = v[s][k];
+        }
+      }
+      if (first) {  // TV(v) guard partials of this tile, consumed by the last pass
+        __shared__ float tsum[NW][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          float x = acc[PT_TVV_R + i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+          if (lane == 0) tsum[w][i] = x;
+        }
+        __syncthreads();
+        if (threadIdx.x < 2) {
+          float t = 0.f;
+          for (int k = 0; k < NW; ++k) t += tsum[k][threadIdx.x];
+          a.tvv[(long long)work * 2 + threadIdx.x] = t;
+        }
+      }
+      __syncthreads();  // band buffers are reused by the next region
+      return;
+    }
+    if (!first && threadIdx.x == 0) {  // TV(v) of this tile from the first pass
+      acc[PT_TVV_R] += a.tvv[(long long)work * 2];
+      acc[PT_TVV_I] += a.tvv[(long long)work * 2 + 1];
     }
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
     const int bf = a.inner & 1;  // not read by the last sweep
@@ -426,7 +489,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   };
   int work = next_from(blockIdx.x);
   if (work < 0) return;
-  if (PF) prefetch_tile(a, pre, work);
+  if (PF && a.t0 == 0) prefetch_tile(a, pre, work);
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nxt = next_from(work + gridDim.x);
     const TileGeom tg = tile_geom(a, work % a.tiles_per_plane);
@@ -444,8 +507,11 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
 int prox_strip_max_halo() { return 14; }
 
 bool prox_strip_applicable(int ny, int nx, int inner) {
-  return ny >= RH && nx >= RW && (nx % 2) == 0 && inner <= 12;
+  (void)inner;  // any T: passes of <= 5 FGP steps beyond T = 8
+  return ny >= RH && nx >= RW && (nx % 2) == 0;
 }
+
+int prox_strip_pass_len(int inner) { return inner > 8 ? 5 : 0; }
 
 // Halo widths.  Garbage from a region edge that is not a plane edge advances
 // one pixel per dependent step: from the top/left edge T B-steps (which read
@@ -458,10 +524,16 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.nx = nx;
   a.P = (long long)ny * nx;
   a.inner = inner;
-  const int h_lo = (inner + 2) & ~1;          // >= T+1, even
-  const int h_hi = inner + (inner & 1);       // >= T, tile even
+  // multi-pass: every pass of <= Tp steps needs lo >= Tp+1 (last pass: Tp
+  // B-steps + the TV statistics) and hi >= Tp+1 (Tp A-steps + the final D^T)
+  const int tp = prox_strip_pass_len(inner);
+  const int h_lo = tp ? ((tp + 2) & ~1) : ((inner + 2) & ~1);  // >= T+1, even
+  const int h_hi = tp ? h_lo : inner + (inner & 1);           // >= T, tile even
   a.halo = h_lo;
   a.tile = RW - h_lo - h_hi;
+  a.pass_len = tp;
+  a.t0 = 0;
+  a.t1 = inner;
   a.tiles_x = (nx + a.tile - 1) / a.tile;
   a.tiles_per_plane = a.tiles_x * ((ny + a.tile - 1) / a.tile);
 }
