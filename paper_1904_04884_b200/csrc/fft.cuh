@@ -1,66 +1,70 @@
-// Shared-memory batched 1D FFTs (power-of-two N, 8..4096), register radix-16
-// Stockham passes.  No host cuFFT anywhere on the hot path.
+// Shared-memory batched 1D FFTs (power-of-two N, 8..4096), register Stockham
+// passes of radix E (16 or 32).  No host cuFFT anywhere on the hot path.
 //
 // Data distribution: the FFT of one line is computed by TPF = N/E threads
-// ("j" = 0..TPF-1), each holding E = min(16, N) elements in registers.  On
-// entry AND on exit thread j holds elements  j + m*TPF,  m = 0..E-1
-// ("natural distribution"), so callers load/store global memory directly
-// from registers with coalesced addresses and can fuse pre/post operations
-// (transfer multiply, scaling, accumulation) element by element.
+// ("j" = 0..TPF-1), each holding E elements in registers.  On entry AND on
+// exit thread j holds elements  j + m*TPF,  m = 0..E-1  ("natural
+// distribution"), so callers load/store global memory directly from registers
+// with coalesced addresses and fuse pre/post operations (transfer multiply,
+// scaling, accumulation) element by element.
 //
-// Passes: radix 16 while N/NS is a multiple of 16, then one pass of the
-// remaining radix (2, 4 or 8).  Between passes the line goes through shared
-// memory; element i of a line lives at buf[pad(i) * S] (S = element stride,
-// 1 for row-contiguous lines, C for C interleaved column lines).  pad(i) =
-// i + i/16 keeps the radix-16 scatter conflict-free.
+// Passes: radix E while N/NS is a multiple of E, then one pass of the
+// remaining radix.  Between passes the line goes through shared memory;
+// element i of a line lives at buf[pad(i) * S] (S = element stride: 1 for
+// row-contiguous lines, C for C interleaved column lines), pad(i) = i + i/E,
+// which keeps the radix-E scatter and the strided reads conflict-free.
+// E = 32 halves the shared-memory exchanges of a 1024-point line (32 x 32:
+// one exchange, one twiddle pass) at the cost of 64 data registers.
 //
 // Sign convention (numpy): forward X[k] = sum x[n] exp(-2 pi i nk/N); the
 // inverse uses +i and is NOT scaled here (callers fold 1/N into their
-// epilogue).  Twiddles come from a table tw[m] = (w, conj w), w = exp(-2 pi i
-// m/N) (fp64-exact entries rounded to fp32) held in shared memory, so a table
-// twiddle multiply is one FMUL2 + one FFMA2.
+// epilogue).  Twiddles come from per-pass tables of (w, conj w), w = exp(-2
+// pi i m/N) (fp64-exact entries rounded to fp32) held in shared memory, so a
+// table twiddle multiply is one FMUL2 + one FFMA2.
 #pragma once
 #include "common.cuh"
 
 namespace holo {
 
 template <int N>
+struct DefaultE {
+  static constexpr int value = N >= 16 ? 16 : N;
+};
+
+template <int N, int EE = DefaultE<N>::value>
 struct FftShape {
   static_assert(N >= 8 && N <= 4096 && (N & (N - 1)) == 0, "N must be a power of two in [8, 4096]");
-  static constexpr int E = N >= 16 ? 16 : N;
+  static_assert(EE <= N && (EE == 8 || EE == 16 || EE == 32 || EE == N), "E must be 8, 16 or 32");
+  static constexpr int E = EE;
   static constexpr int TPF = N / E;
+  static constexpr int SH = E == 32 ? 5 : E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;  // log2 E
   // padded line length in elements; the +2/+TPF term staggers consecutive
-  // lines across banks (see kernels: lines of one warp start on distinct banks)
-  static constexpr int PADN = N + N / 16 + (TPF >= 16 ? 2 : TPF);
+  // lines across banks (lines of one warp start on distinct banks)
+  static constexpr int PADN = N + N / E + (TPF >= 16 ? 2 : TPF);
 };
 
 // Twiddle tables are stored per pass as [r-1][kk] (kk = butterfly index mod
 // NS), so the lanes of a warp (consecutive kk) read consecutive entries:
 // conflict-free, or broadcast.  Entry = (w, conj w), w = exp(-2 pi i kk r/(NS R)).
-template <int N>
+template <int N, int E = DefaultE<N>::value>
 struct TwLayout {
-  static constexpr int radix(int ns) { return ((N / ns) % 16 == 0) ? 16 : N / ns; }
+  static constexpr int radix(int ns) { return ((N / ns) % E == 0) ? E : N / ns; }
   // offset of the table of the pass whose product of earlier radices is ns
   static constexpr int offset(int ns) {
     int off = 0;
-    for (int s = 16; s < ns; s *= radix(s)) off += (radix(s) - 1) * s;
+    for (int s = E; s < ns; s *= radix(s)) off += (radix(s) - 1) * s;
     return off;
   }
   static constexpr int size() {
-    if (N <= 16) return 1;
+    if (N <= E) return 1;
     int off = 0;
-    for (int s = 16; s < N; s *= radix(s)) off += (radix(s) - 1) * s;
+    for (int s = E; s < N; s *= radix(s)) off += (radix(s) - 1) * s;
     return off;
   }
 };
 
-HD int fft_pad(int i) { return i + (i >> 4); }
-// pad(i + d) - pad(i) for a compile-time d that is a multiple of 16 (any i >= 0)
-template <int D>
-struct PadStep {
-  static_assert(D % 16 == 0, "");
-  static constexpr int value = D + D / 16;
-};
+template <int SH>
+HD int fft_pad(int i) { return i + (i >> SH); }
 
 // Complex arithmetic on packed f32x2 pairs (FADD2/FMUL2/FFMA2); the (re, im)
 // swap below compiles to the .LO_HI operand selector, not a move.
@@ -94,30 +98,46 @@ HD void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
   a3 = add_ni<!INV>(t1, t3);
 }
 
-// x * exp(-/+ 2 pi i e / 16), e in [0, 16) compile-time
+// cos / sin of pi k / 16, k = 0..15 (fp64 values rounded to fp32)
+struct Trig32 {
+  static constexpr float c[16] = {1.0f, 0.98078528040323043f, 0.92387953251128674f, 0.83146961230254524f,
+                                  0.70710678118654757f, 0.55557023301960229f, 0.38268343236508984f,
+                                  0.19509032201612833f, 0.0f, -0.19509032201612819f, -0.38268343236508973f,
+                                  -0.55557023301960196f, -0.70710678118654746f, -0.83146961230254535f,
+                                  -0.92387953251128674f, -0.98078528040323043f};
+  static constexpr float s[16] = {0.0f, 0.19509032201612825f, 0.38268343236508978f, 0.55557023301960218f,
+                                  0.70710678118654746f, 0.83146961230254524f, 0.92387953251128674f,
+                                  0.98078528040323043f, 1.0f, 0.98078528040323043f, 0.92387953251128674f,
+                                  0.83146961230254546f, 0.70710678118654757f, 0.55557023301960218f,
+                                  0.38268343236508989f, 0.19509032201612861f};
+};
+
+// x * exp(-/+ 2 pi i e / 32), e compile-time
 template <bool INV, int e>
-HD float2 rot16(float2 x) {
-  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508978f, R2 = 0.70710678118654752f;
-  constexpr int ee = e & 15;
+HD float2 rot32(float2 x) {
+  constexpr int ee = e & 31;
   if constexpr (ee == 0) {
     return x;
-  } else if constexpr (ee == 4) {
-    return mul_ni<INV>(x);
   } else if constexpr (ee == 8) {
+    return mul_ni<INV>(x);
+  } else if constexpr (ee == 16) {
     return make_float2(-x.x, -x.y);
-  } else if constexpr (ee == 12) {
+  } else if constexpr (ee == 24) {
     return mul_ni<!INV>(x);
   } else {
-    // cos/sin of pi*ee/8
-    constexpr float cs = (ee == 1 || ee == 15) ? C1 : (ee == 2 || ee == 14) ? R2 : (ee == 3 || ee == 13) ? S1
-                       : (ee == 5 || ee == 11) ? -S1 : (ee == 6 || ee == 10) ? -R2 : -C1;
-    constexpr float sn = (ee == 1 || ee == 7) ? S1 : (ee == 2 || ee == 6) ? R2 : (ee == 3 || ee == 5) ? C1
-                       : (ee == 9 || ee == 15) ? -S1 : (ee == 10 || ee == 14) ? -R2 : -C1;
+    // angle pi ee / 16 in [0, 2 pi): the second half-turn negates the first
+    constexpr int h = ee & 15;
+    constexpr float cs = (ee < 16) ? Trig32::c[h] : -Trig32::c[h];
+    constexpr float sn = (ee < 16) ? Trig32::s[h] : -Trig32::s[h];
     // forward: multiply by (cs, -sn); inverse: (cs, +sn)
     //   x (cs + i s) = x * cs + swap(x) * (-s, s)
     constexpr float s = INV ? sn : -sn;
     return fma2(swp(x), make_float2(-s, s), mul2(x, make_float2(cs, cs)));
   }
+}
+template <bool INV, int e>
+HD float2 rot16(float2 x) {
+  return rot32<INV, 2 * e>(x);
 }
 
 // a * w (forward) or a * conj(w) (inverse) with the table entry t = (w, conj w):
@@ -182,20 +202,46 @@ struct Dft<16, INV> {
     for (int i = 0; i < 16; ++i) a[i] = t[i];
   }
 };
+// 32 = 2 x 16: DFT16 of the even and odd samples, X[k] = E[k] +- w32^k O[k].
+template <bool INV>
+struct Dft<32, INV> {
+  template <int K>
+  static HD void combine(float2 (&ev)[16], float2 (&od)[16], float2 (&a)[32]) {
+    if constexpr (K < 16) {
+      const float2 o = rot32<INV, K>(od[K]);
+      a[K] = add2(ev[K], o);
+      a[K + 16] = sub2(ev[K], o);
+      combine<K + 1>(ev, od, a);
+    }
+  }
+  static HD void run(float2 (&a)[32]) {
+    float2 ev[16], od[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      ev[i] = a[2 * i];
+      od[i] = a[2 * i + 1];
+    }
+    Dft<16, INV>::run(ev);
+    Dft<16, INV>::run(od);
+    combine<0>(ev, od, a);
+  }
+};
 
 // One Stockham pass of radix R with NS = product of earlier radices.
-template <int N, int R, int NS, bool INV, bool FIRST, bool LAST>
-HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
-  constexpr int E = FftShape<N>::E, TPF = FftShape<N>::TPF, BPT = E / R;
+template <int N, int E, int R, int NS, bool INV, bool FIRST, bool LAST>
+HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __restrict__ tw) {
+  using Sh = FftShape<N, E>;
+  constexpr int TPF = Sh::TPF, BPT = E / R, SH = Sh::SH;
   static_assert(E % R == 0, "radix must divide E");
   if constexpr (!FIRST) {
-    if constexpr (TPF % 16 == 0) {
-      const float2* rp = buf + fft_pad(j) * S;  // one address, immediate offsets
+    if constexpr (TPF % E == 0) {
+      // pad(j + m TPF) = pad(j) + m (TPF + TPF/E): one address, immediate offsets
+      const float2* rp = buf + fft_pad<SH>(j) * S;
 #pragma unroll
-      for (int m = 0; m < E; ++m) v[m] = rp[m * PadStep<TPF>::value * S];
+      for (int m = 0; m < E; ++m) v[m] = rp[m * (TPF + TPF / E) * S];
     } else {
 #pragma unroll
-      for (int m = 0; m < E; ++m) v[m] = buf[fft_pad(j + m * TPF) * S];
+      for (int m = 0; m < E; ++m) v[m] = buf[fft_pad<SH>(j + m * TPF) * S];
     }
     if constexpr (!LAST) __syncthreads();  // everyone has read before anyone writes
   } else if constexpr (!LAST) {
@@ -209,7 +255,7 @@ HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const f
     for (int r = 0; r < R; ++r) a[r] = v[s + r * BPT];
     if constexpr (NS > 1) {
       const int kk = b % NS;
-      const float4* tp = tw + TwLayout<N>::offset(NS) + kk;
+      const float4* tp = tw + TwLayout<N, E>::offset(NS) + kk;
       // groups of 4 twiddles: bounds the 4-register table entries in flight
 #pragma unroll
       for (int r0 = 1; r0 < R; r0 += 4) {
@@ -224,36 +270,36 @@ HD void fft_pass(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const f
       for (int r = 0; r < R; ++r) v[s + r * BPT] = a[r];
     } else {
       const int base = (b / NS) * NS * R + (b % NS);
-      float2* wp = buf + fft_pad(base) * S;
-      if constexpr (NS % 16 == 0) {
+      float2* wp = buf + fft_pad<SH>(base) * S;
+      if constexpr (NS % E == 0) {  // pad(base + r NS) = pad(base) + r (NS + NS/E)
 #pragma unroll
-        for (int r = 0; r < R; ++r) wp[r * PadStep<NS>::value * S] = a[r];
-      } else if constexpr (NS == 1 && R == 16) {  // base = 16 b: pad(base + r) = pad(base) + r
+        for (int r = 0; r < R; ++r) wp[r * (NS + NS / E) * S] = a[r];
+      } else if constexpr (NS == 1 && R == E) {  // base = E b: pad(base + r) = pad(base) + r
 #pragma unroll
         for (int r = 0; r < R; ++r) wp[r * S] = a[r];
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[fft_pad(base + r * NS) * S] = a[r];
+        for (int r = 0; r < R; ++r) buf[fft_pad<SH>(base + r * NS) * S] = a[r];
       }
     }
   }
   if constexpr (!LAST) __syncthreads();
 }
 
-template <int N, int NS, bool INV, bool FIRST>
-HD void fft_passes(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
+template <int N, int E, int NS, bool INV, bool FIRST>
+HD void fft_passes(float2 (&v)[E], int j, float2* buf, int S, const float4* __restrict__ tw) {
   constexpr int REM = N / NS;
-  constexpr int R = (REM % 16 == 0) ? 16 : REM;
+  constexpr int R = (REM % E == 0) ? E : REM;
   constexpr bool LAST = (NS * R == N);
-  fft_pass<N, R, NS, INV, FIRST, LAST>(v, j, buf, S, tw);
-  if constexpr (!LAST) fft_passes<N, NS * R, INV, false>(v, j, buf, S, tw);
+  fft_pass<N, E, R, NS, INV, FIRST, LAST>(v, j, buf, S, tw);
+  if constexpr (!LAST) fft_passes<N, E, NS * R, INV, false>(v, j, buf, S, tw);
 }
 
 // Full length-N transform of the line held by the TPF threads j=0..TPF-1.
 // Contains __syncthreads(): every thread of the block must call it.
-template <int N, bool INV>
-HD void fft_line(float2 (&v)[FftShape<N>::E], int j, float2* buf, int S, const float4* __restrict__ tw) {
-  fft_passes<N, 1, INV, true>(v, j, buf, S, tw);
+template <int N, bool INV, int E = DefaultE<N>::value>
+HD void fft_line(float2 (&v)[E], int j, float2* buf, int S, const float4* __restrict__ tw) {
+  fft_passes<N, E, 1, INV, true>(v, j, buf, S, tw);
 }
 
 }  // namespace holo

@@ -49,17 +49,26 @@ bool dispatch_n(int n, F&& f) {
 
 inline int col_width(int ny) { return ny >= 4096 ? 4 : 8; }
 
+// elements per thread: 32 (one shared-memory exchange per 1024-point line)
+// where registers allow; the accumulating forward column pass keeps 16
+template <int N>
+struct EBig {
+  static constexpr int value = N >= 512 ? 32 : DefaultE<N>::value;
+};
+template <int E>
+constexpr int tw_slot() { return E == 32 ? 1 : 0; }
+
 // ------------------------------------------------------------ K1 tables ----
 
 // per-pass twiddle tables (TwLayout): entry (r-1)*NS + kk of the pass with
 // product-of-earlier-radices NS holds w = exp(-2 pi i kk r / (NS R)) as (w, conj w)
-template <int N>
+template <int N, int E>
 __global__ void k_twiddles(float4* tw) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= TwLayout<N>::size()) return;
+  if (e >= TwLayout<N, E>::size()) return;
   int off = 0;
-  for (int ns = 16; ns < N; ns *= TwLayout<N>::radix(ns)) {
-    const int R = TwLayout<N>::radix(ns);
+  for (int ns = E; ns < N; ns *= TwLayout<N, E>::radix(ns)) {
+    const int R = TwLayout<N, E>::radix(ns);
     if (e < off + (R - 1) * ns) {
       const int r = 1 + (e - off) / ns, kk = (e - off) % ns;
       double sn, cs;
@@ -111,16 +120,16 @@ __global__ void k_phase(uint64_t* tab, uint8_t* mask, int ny, int nx, double pit
 
 // ------------------------------------------------------------- K3 rows -----
 
-template <int N, bool INV>
+template <int N, bool INV, int E_>
 __global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
                                                           long long nrows, float scale, const float4* __restrict__ twg) {
-  using Sh = FftShape<N>;
+  using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int RPC = kRowThreads / TPF;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* buf = smem + 2 * N;
-  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   __syncthreads();
   const int lr = threadIdx.x / TPF, j = threadIdx.x % TPF;
   for (long long row0 = (long long)blockIdx.x * RPC; row0 < nrows; row0 += (long long)gridDim.x * RPC) {
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restri
     const float2* src = in + row * N + j;
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = active ? src[m * TPF] : czero();
-    fft_line<N, INV>(v, j, buf + lr * Sh::PADN, 1, tw);
+    fft_line<N, INV, E_>(v, j, buf + lr * Sh::PADN, 1, tw);
     if (active) {
       float2* dst = out + row * N + j;
       const float2 sc = splat2(scale);
@@ -145,16 +154,16 @@ __global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restri
 // Element m of thread (j, c) is row j + m*TPF.  Lanes vary fastest in c, so a
 // warp loads C-wide contiguous row segments.
 
-template <int N, bool INV, int C>
-__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fft_cols(const float2* __restrict__ in,
+template <int N, bool INV, int C, int E_>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const float2* __restrict__ in,
                                                                     float2* __restrict__ out, int nx, long long P,
                                                                     float scale, const float4* __restrict__ twg) {
-  using Sh = FftShape<N>;
+  using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* buf = smem + 2 * N;
-  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
@@ -163,25 +172,25 @@ __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fft_cols(const float2*
   float2 v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = in[base + m * st];
-  fft_line<N, INV>(v, j, buf + c, C, tw);
+  fft_line<N, INV, E_>(v, j, buf + c, C, tw);
 #pragma unroll
   for (int m = 0; m < E; ++m) out[base + m * st] = cscale(v[m], scale);
 }
 
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
-template <int N, int C>
-__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_adj_cols(const float2* __restrict__ R,
+template <int N, int C, int E_>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const float2* __restrict__ R,
                                                                     float2* __restrict__ out, int nx, long long P,
                                                                     int k0, const uint64_t* __restrict__ tab,
                                                                     const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
-  using Sh = FftShape<N>;
+  using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* circ = smem + 2 * N;
   float2* buf = smem + 2 * N + 256;
-  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
@@ -191,27 +200,27 @@ __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_adj_cols(const float2*
   float2 v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ));
-  fft_line<N, true>(v, j, buf + c, C, tw);
+  fft_line<N, true, E_>(v, j, buf + c, C, tw);
   float2* dst = out + (long long)k * P + p0;
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = v[m];
 }
 
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
-template <int N, int C>
-__global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fwd_cols(const float2* __restrict__ in,
+template <int N, int C, int E_>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const float2* __restrict__ in,
                                                                     float2* __restrict__ Spart, int nx, long long P,
                                                                     int nzl, int ppg, int k0,
                                                                     const uint64_t* __restrict__ tab,
                                                                     const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
-  using Sh = FftShape<N>;
+  using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* circ = smem + 2 * N;
   float2* buf = smem + 2 * N + 256;
-  for (int i = threadIdx.x; i < TwLayout<N>::size(); i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(C * FftShape<N>::TPF) k_fwd_cols(const float2*
     const float2* src = in + (long long)k * P + p0;
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = src[m * st];
-    fft_line<N, false>(v, j, buf + c, C, tw);
+    fft_line<N, false, E_>(v, j, buf + c, C, tw);
     // transfer multiply-accumulate in chunks of 4: bounds the table loads in
     // flight (16 B each) so acc[] + v[] stay in registers
 #pragma unroll
@@ -393,8 +402,8 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
         if (er > 0) { gyr = uor - ur[idx - EW]; gyi = uoi - ui[idx - EW]; }
         if (ec > 0) { gxr = uor - ur[idx - 1]; gxi = uoi - ui[idx - 1]; }
         if (t == 0 && er >= ei0 && er < ei1 && ec >= ej0 && ec < ej1) {
-          acc[PT_TVV_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
-          acc[PT_TVV_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
+          acc[PT_G_R] -= (double)tau * sqrtf(gyr * gyr + gxr * gxr);
+          acc[PT_G_I] -= (double)tau * sqrtf(gyi * gyi + gxi * gxi);
         }
         float opr = 0.f, opi = 0.f, oqr = 0.f, oqi = 0.f;
         if (t > 0) { opr = rpr[idx]; opi = rpi[idx]; oqr = rqr[idx]; oqi = rqi[idx]; }
@@ -457,11 +466,9 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
       float gyr = 0.f, gyi = 0.f, gxr = 0.f, gxi = 0.f;
       if (er > 0) { gyr = wr - ur[idx - EW]; gyi = wi - ui[idx - EW]; }
       if (ec > 0) { gxr = wr - ur[idx - 1]; gxi = wi - ui[idx - 1]; }
-      acc[PT_TVW_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
-      acc[PT_TVW_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
       const float dr = wr - vr[m], di = wi - vi[m];
-      acc[PT_D2_R] += (double)(dr * dr);
-      acc[PT_D2_I] += (double)(di * di);
+      acc[PT_G_R] += (double)tau * sqrtf(gyr * gyr + gxr * gxr) + 0.5 * (double)(dr * dr);
+      acc[PT_G_I] += (double)tau * sqrtf(gyi * gyi + gxi * gxi) + 0.5 * (double)(di * di);
     }
     if (force & 1u) wr = vr[m];
     if (force & 2u) wi = vi[m];
@@ -501,8 +508,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     float gyr = 0.f, gyi = 0.f, gxr = 0.f, gxi = 0.f;
     if (er > 0) { gyr = xr - rpr[idx - EW]; gyi = xi - rpi[idx - EW]; }
     if (ec > 0) { gxr = xr - rpr[idx - 1]; gxi = xi - rpi[idx - 1]; }
-    acc[PT_TVX_R] += (double)sqrtf(gyr * gyr + gxr * gxr);
-    acc[PT_TVX_I] += (double)sqrtf(gyi * gyi + gxi * gxi);
+    acc[PT_TVX] += (double)sqrtf(gyr * gyr + gxr * gxr) + (double)sqrtf(gyi * gyi + gxi * gxi);
     acc[PT_L1] += (double)hypotf(xr, xi);
     const long long g = pbase + (long long)(ri0 + er) * a.nx + (rj0 + ec);
     float2 y = a.x[g];
@@ -543,8 +549,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
     uint32_t bits = 0;
     if (tv_on) {
       // prox.py:138-147: reject the TV output when tau TV(w) + |w-v|^2/2 > tau TV(v)
-      if (tau * s[PT_TVW_R] + 0.5 * s[PT_D2_R] > tau * s[PT_TVV_R]) bits |= 1u;
-      if (tau * s[PT_TVW_I] + 0.5 * s[PT_D2_I] > tau * s[PT_TVV_I]) bits |= 2u;
+      if (s[PT_G_R] > 0.0) bits |= 1u;
+      if (s[PT_G_I] > 0.0) bits |= 2u;
     }
     const uint32_t old = force_acc[plane];
     force_acc[plane] = (uint8_t)(old | bits);
@@ -553,7 +559,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
     o[0] = s[PT_IP];
     o[1] = s[PT_DX2];
     o[2] = s[PT_L1];
-    o[3] = s[PT_TVX_R] + s[PT_TVX_I];
+    o[3] = s[PT_TVX];
   }
 }
 
@@ -769,19 +775,24 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
   p.pitch = pitch; p.dz = dz; p.z0 = z0; p.lam = lam;
   p.col_c = col_width(ny);
   cudaError_t e;
-  if ((e = cudaMalloc(&p.tw_x, sizeof(float4) * std::max(nx, 16)))) return e;
-  if ((e = cudaMalloc(&p.tw_y, sizeof(float4) * std::max(ny, 16)))) return e;
+  for (int k = 0; k < 2; ++k) {
+    if ((e = cudaMalloc(&p.tw_x[k], sizeof(float4) * std::max(nx, 32)))) return e;
+    if ((e = cudaMalloc(&p.tw_y[k], sizeof(float4) * std::max(ny, 32)))) return e;
+  }
   if ((e = cudaMalloc(&p.circle, sizeof(float2) * 256))) return e;
   if ((e = cudaMalloc(&p.phase, sizeof(uint64_t) * p.P))) return e;
   if ((e = cudaMalloc(&p.mask, p.P))) return e;
-  dispatch_n(nx, [&](auto nc) {
-    constexpr int N = decltype(nc)::value;
-    k_twiddles<N><<<(TwLayout<N>::size() + 255) / 256, 256, 0, s>>>(p.tw_x);
-  });
-  dispatch_n(ny, [&](auto nc) {
-    constexpr int N = decltype(nc)::value;
-    k_twiddles<N><<<(TwLayout<N>::size() + 255) / 256, 256, 0, s>>>(p.tw_y);
-  });
+  // one table layout per element count: [0] E = 16 (or N), [1] E = 32 (or the E=16 one)
+  auto tables = [&](int n, float4** tw) {
+    dispatch_n(n, [&](auto nc) {
+      constexpr int N = decltype(nc)::value;
+      constexpr int E0 = DefaultE<N>::value, E1 = EBig<N>::value;
+      k_twiddles<N, E0><<<(TwLayout<N, E0>::size() + 255) / 256, 256, 0, s>>>(tw[0]);
+      k_twiddles<N, E1><<<(TwLayout<N, E1>::size() + 255) / 256, 256, 0, s>>>(tw[1]);
+    });
+  };
+  tables(nx, p.tw_x);
+  tables(ny, p.tw_y);
   COUNT_LAUNCH(2);
   k_circle<<<1, 256, 0, s>>>(p.circle);
   COUNT_LAUNCH(1);
@@ -794,8 +805,12 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
 }
 
 void plan_free(Plan& p) {
-  cudaFree(p.tw_x); cudaFree(p.tw_y); cudaFree(p.circle); cudaFree(p.phase); cudaFree(p.mask);
-  p.tw_x = p.tw_y = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(p.tw_x[k]);
+    cudaFree(p.tw_y[k]);
+    p.tw_x[k] = p.tw_y[k] = nullptr;
+  }
+  cudaFree(p.circle); cudaFree(p.phase); cudaFree(p.mask);
   p.circle = nullptr;
   p.phase = nullptr;
   p.mask = nullptr;
@@ -812,17 +827,18 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.nx, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
-    using Sh = FftShape<N>;
+    constexpr int E = EBig<N>::value;
+    using Sh = FftShape<N, E>;
     constexpr int RPC = kRowThreads / Sh::TPF;
     const size_t smem = sizeof(float2) * (2 * N + (size_t)RPC * Sh::PADN);
     const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
     if (inverse) {
-      err = set_smem(k_fft_rows<N, true>, smem);
-      k_fft_rows<N, true><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x);
+      err = set_smem(k_fft_rows<N, true, E>, smem);
+      k_fft_rows<N, true, E><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
   COUNT_LAUNCH(1);
     } else {
-      err = set_smem(k_fft_rows<N, false>, smem);
-      k_fft_rows<N, false><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x);
+      err = set_smem(k_fft_rows<N, false, E>, smem);
+      k_fft_rows<N, false, E><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
   COUNT_LAUNCH(1);
     }
   });
@@ -830,9 +846,9 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
   return err ? err : cudaGetLastError();
 }
 
-template <int N, int C>
+template <int N, int C, int E>
 static size_t col_smem(int extra) {
-  return sizeof(float2) * (2 * N + extra + (size_t)(N + N / 16) * C);
+  return sizeof(float2) * (2 * N + extra + (size_t)(N + N / E) * C);
 }
 
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
@@ -840,19 +856,19 @@ cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, 
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
+    constexpr int E = DefaultE<N>::value;  // radix-32 columns measured slower (occupancy)
     constexpr int C = N >= 4096 ? 4 : 8;
-    constexpr int NT = C * FftShape<N>::TPF;
-    const size_t smem = col_smem<N, C>(0);
+    constexpr int NT = C * FftShape<N, E>::TPF;
+    const size_t smem = col_smem<N, C, E>(0);
     dim3 grid(p.nx / C, nplanes);
     if (inverse) {
-      err = set_smem(k_fft_cols<N, true, C>, smem);
-      k_fft_cols<N, true, C><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y);
-  COUNT_LAUNCH(1);
+      err = set_smem(k_fft_cols<N, true, C, E>, smem);
+      k_fft_cols<N, true, C, E><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y[tw_slot<E>()]);
     } else {
-      err = set_smem(k_fft_cols<N, false, C>, smem);
-      k_fft_cols<N, false, C><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y);
-  COUNT_LAUNCH(1);
+      err = set_smem(k_fft_cols<N, false, C, E>, smem);
+      k_fft_cols<N, false, C, E><<<grid, NT, smem, s>>>(in, out, p.nx, p.P, scale, p.tw_y[tw_slot<E>()]);
     }
+    COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
   return err ? err : cudaGetLastError();
@@ -862,12 +878,13 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
+    constexpr int E = DefaultE<N>::value;  // radix-32 columns measured slower (occupancy)
     constexpr int C = N >= 4096 ? 4 : 8;
-    constexpr int NT = C * FftShape<N>::TPF;
-    const size_t smem = col_smem<N, C>(256);
+    constexpr int NT = C * FftShape<N, E>::TPF;
+    const size_t smem = col_smem<N, C, E>(256);
     dim3 grid(p.nx / C, nzl);
-    err = set_smem(k_adj_cols<N, C>, smem);
-    k_adj_cols<N, C><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y, p.circle);
+    err = set_smem(k_adj_cols<N, C, E>, smem);
+    k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
   COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
@@ -886,12 +903,14 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
-    constexpr int C = 4;  // acc[] + v[] per thread: 256-thread CTAs keep them in registers
-    constexpr int NT = C * FftShape<N>::TPF;
-    const size_t smem = col_smem<N, C>(256);
+    constexpr int E = DefaultE<N>::value;  // acc[] + v[] per thread
+    constexpr int C = 4;  // 256-thread CTAs keep acc[] + v[] in registers
+    constexpr int NT = C * FftShape<N, E>::TPF;
+    const size_t smem = col_smem<N, C, E>(256);
     dim3 grid(p.nx / C, groups);
-    err = set_smem(k_fwd_cols<N, C>, smem);
-    k_fwd_cols<N, C><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y, p.circle);
+    err = set_smem(k_fwd_cols<N, C, E>, smem);
+    k_fwd_cols<N, C, E><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
+                                                p.circle);
   COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
@@ -952,7 +971,7 @@ bool prox_supported(int ny, int nx, int inner) {
 
 cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
   if (a.kind == 1) {
-    if (!a.pass_len) {
+    if (!a.pass_len || !(a.tau_tv > 0.f)) {  // no TV: nothing to split into passes
       COUNT_LAUNCH(1);
       return prox_strip(a, s);
     }

@@ -11,17 +11,19 @@ struct Plan {
   long long P = 0;             // ny * nx
   double pitch = 0, dz = 0, z0 = 0, lam = 0;
   int col_c = 8;                // interleaved columns per column-pass CTA
-  float4* tw_x = nullptr;       // (w, conj w), w = exp(-2 pi i m / nx), m < nx
-  float4* tw_y = nullptr;       // same for ny
+  float4* tw_x[2] = {nullptr, nullptr};  // per-pass (w, conj w) tables for nx: [0] E=16, [1] E=32
+  float4* tw_y[2] = {nullptr, nullptr};  // same for ny
   float2* circle = nullptr;     // exp(2 pi i m / 256)
   uint64_t* phase = nullptr;    // per pixel packed (frac(z0 q), frac(dz q)) cycle fractions (plane_phase)
   uint8_t* mask = nullptr;      // per pixel 1 = propagating (arg >= 0)
   int any_propagating = 0;
 };
 
-constexpr int kProxParts = 11;  // per-tile fp64 partial sums written by the prox kernel
+constexpr int kProxParts = 6;  // per-tile fp64 partial sums written by the prox kernel
 // indices into a tile's partials
-enum ProxPart { PT_TVW_R = 0, PT_TVW_I, PT_D2_R, PT_D2_I, PT_TVV_R, PT_TVV_I, PT_IP, PT_DX2, PT_L1, PT_TVX_R, PT_TVX_I };
+// G = tau TV(w) + |w - v|^2 / 2 - tau TV(v) per (re, im) part: the TV guard
+// (prox.py:138-147) fires where G > 0; TVX = TV(Re x_new) + TV(Im x_new)
+enum ProxPart { PT_G_R = 0, PT_G_I, PT_IP, PT_DX2, PT_L1, PT_TVX };
 
 struct ProxArgs {
   const float2* x = nullptr;     // state x_k

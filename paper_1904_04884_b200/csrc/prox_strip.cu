@@ -38,9 +38,13 @@ constexpr int SR = HOLO_PROX_SR;  // rows per thread (2: 1024 threads / 64 regs;
 constexpr int NW = RH / SR;       // warps = row bands
 constexpr int NT = 32 * NW;
 
+// Band w publishes top[.][w] and bot[w + 1]; it reads top[.][w + 1] (band
+// below) and bot[w] (band above).  top[.][NW] and bot[0] are never written:
+// interior regions read them as garbage for the region's outer rows (halo),
+// so the read needs no select; plane-edge regions (EDGE) apply the exact rule.
 struct Bands {
-  float4 top[2][NW][RW / 2];  // [buf][band][lane]: row-0 values (2 columns) -> down neighbour of the band above
-  float4 bot[NW][RW / 2];     // row-(SR-1) values -> up neighbour of the band below
+  float4 top[2][NW + 1][RW / 2];  // [buf][band][lane]: row-0 values (2 columns) -> down neighbour of the band above
+  float4 bot[NW + 1][RW / 2];     // row-(SR-1) values -> up neighbour of the band below
 };
 
 HD float4 f4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
@@ -107,13 +111,13 @@ HD void prefetch_tile(const ProxArgs& a, float4* pre, int work) {
 
 // One 64x64 region.  Inputs come from this thread's prefetch slots; the
 // prefetch of `next_work` (if >= 0) is issued as soon as the slots are read.
-// EDGE: the region touches the plane's left or right edge, so its outer
-// columns need the exact replicated-edge rule; otherwise they are garbage
-// zone and the lane-0 / lane-31 selects are skipped.
+// EDGE: the region touches a plane edge, so its outer rows/columns need the
+// exact replicated-edge rule; otherwise they are garbage zone and the
+// lane-0 / lane-31 / band-0 / band-(NW-1) selects are skipped.
 // prefetch through shared memory only when the smem budget allows the double buffer
 constexpr bool PF = (SR >= 4);
 
-template <bool TV, bool EDGE>
+template <bool TV, bool EDGE, bool MP>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, float4* pre_next, int work,
                                           int next_work) {
   const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
@@ -137,8 +141,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   const long long g0 = strip_base(a, plane, tg);
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
-  const bool first = a.t0 == 0, last = a.t1 >= a.inner;
-  const int pass = a.pass_len ? a.t0 / a.pass_len : 0;
+  // MP: multi-pass launch (compile-time, so the single-pass kernel carries no pass state)
+  const bool first = !MP || a.t0 == 0, last = !MP || a.t1 >= a.inner;
+  const int pass = MP ? a.t0 / a.pass_len : 0;
   // state halves alternate by pass parity so a pass never overwrites what
   // neighbouring regions of the same launch still read as their halo
   const float4* s_in = a.sbuf + ((pass - 1) & 1) * a.sstride;
@@ -206,17 +211,18 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     return r;
   };
   auto above_of = [&](int k, float2 self) -> float2 {
-    if (w == 0) return self;  // region top row: zero y-difference
-    const float4 b4 = sm.bot[w - 1][lane];
+    if (EDGE && w == 0) return self;  // region top row: zero y-difference
+    const float4 b4 = sm.bot[w][lane];
     return k ? hi2(b4) : lo2(b4);
   };
   const float2 mtau = splat2(-a.tau_tv);
+  const float ttv = a.tau_tv;
 
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
     if (first) {
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
-    sm.bot[w][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
+    sm.bot[w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     __syncthreads();
     {
       float2 up0 = above_of(0, v[0][0]), up1 = above_of(1, v[0][1]);
@@ -227,15 +233,16 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         const float2 gy0 = sub2(v[s][0], up0), gy1 = sub2(v[s][1], up1);
         up0 = v[s][0];
         up1 = v[s][1];
+        // guard: G = tau TV(w) + |w - v|^2 / 2 - tau TV(v) per part, here the -tau TV(v) term
         if (mInt & (1u << (2 * s))) {
           const float2 nv = norm_pair(gy0, gx0);
-          acc[PT_TVV_R] += nv.x;
-          acc[PT_TVV_I] += nv.y;
+          acc[PT_G_R] = fmaf(-ttv, nv.x, acc[PT_G_R]);
+          acc[PT_G_I] = fmaf(-ttv, nv.y, acc[PT_G_I]);
         }
         if (mInt & (2u << (2 * s))) {
           const float2 nv = norm_pair(gy1, gx1);
-          acc[PT_TVV_R] += nv.x;
-          acc[PT_TVV_I] += nv.y;
+          acc[PT_G_R] = fmaf(-ttv, nv.x, acc[PT_G_R]);
+          acc[PT_G_I] = fmaf(-ttv, nv.y, acc[PT_G_I]);
         }
         float2 pn0 = mul2(lr2, gy0), qn0 = mul2(lr2, gx0);
         float2 pn1 = mul2(lr2, gy1), qn1 = mul2(lr2, gx1);
@@ -254,6 +261,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       __syncthreads();
     }
     // ---- iterations max(t0,1)..t1-1: one fused sweep down the band per iteration ----
+#pragma unroll 2
     for (int t = first ? 1 : a.t0; t < a.t1; ++t) {
       const int b = (t - 1) & 1;  // buffer holding this iteration's band-top rp
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
@@ -266,10 +274,10 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       // pre-pass: the band's last row, needed by the band below before its sweep
       float2 ul0, ul1;
       {
-        const float4 d4 = (w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
         urow(SR - 1, lo2(d4), hi2(d4), ul0, ul1);
       }
-      sm.bot[w][lane] = f4(ul0, ul1);
+      sm.bot[w + 1][lane] = f4(ul0, ul1);
       __syncthreads();
       float2 up0 = above_of(0, make_float2(0.f, 0.f)), up1 = above_of(1, make_float2(0.f, 0.f));
 #pragma unroll
@@ -281,7 +289,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         } else {
           urow(s, rp[s + 1][0], rp[s + 1][1], u0, u1);
         }
-        if (s == 0 && w == 0) {  // region top row: zero y-difference
+        if (EDGE && s == 0 && w == 0) {  // region top row: zero y-difference
           up0 = u0;
           up1 = u1;
         }
@@ -323,7 +331,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         __shared__ float tsum[NW][2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          float x = acc[PT_TVV_R + i];
+          float x = acc[PT_G_R + i];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
           if (lane == 0) tsum[w][i] = x;
@@ -339,15 +347,15 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       return;
     }
     if (!first && threadIdx.x == 0) {  // TV(v) of this tile from the first pass
-      acc[PT_TVV_R] += a.tvv[(long long)work * 2];
-      acc[PT_TVV_I] += a.tvv[(long long)work * 2 + 1];
+      acc[PT_G_R] += a.tvv[(long long)work * 2];
+      acc[PT_G_I] += a.tvv[(long long)work * 2 + 1];
     }
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
     const int bf = a.inner & 1;  // not read by the last sweep
     sm.top[bf][w][lane] = f4(p[0][0], p[0][1]);
     __syncthreads();
     {
-      const float4 d4 = (w < NW - 1) ? sm.top[bf][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[bf][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         const float2 pd0 = (s < SR - 1) ? p[s + 1][0] : lo2(d4);
@@ -357,7 +365,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         rp[s][1] = fma2(mtau, sub2(sub2(add2(p[s][1], q[s][1]), pd1), qr1), v[s][1]);
       }
     }
-    sm.bot[w][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
+    sm.bot[w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
@@ -374,10 +382,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
           if (mInt & (1u << (2 * s + k))) {
             const float2 nw = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
             const float2 dv = sub2(rp[s][k], v[s][k]);
-            acc[PT_TVW_R] += nw.x;
-            acc[PT_TVW_I] += nw.y;
-            acc[PT_D2_R] += dv.x * dv.x;
-            acc[PT_D2_I] += dv.y * dv.y;
+            acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f * dv.x, dv.x, acc[PT_G_R]));
+            acc[PT_G_I] = fmaf(ttv, nw.y, fmaf(0.5f * dv.y, dv.y, acc[PT_G_I]));
           }
         }
       }
@@ -409,7 +415,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       p[s][k] = make_float2(wr * gsc, wi * gsc);
     }
   }
-  sm.bot[w][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+  sm.bot[w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
   __syncthreads();
   {
     float2 up0 = above_of(0, p[0][0]), up1 = above_of(1, p[0][1]);
@@ -439,8 +445,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       for (int k = 0; k < 2; ++k) {
         if (!(rowbits & (1u << k))) continue;
         const float2 nx2 = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
-        acc[PT_TVX_R] += nx2.x;
-        acc[PT_TVX_I] += nx2.y;
+        acc[PT_TVX] += nx2.x + nx2.y;
         acc[PT_L1] += sqrt_a(fmaf(p[s][k].x, p[s][k].x, p[s][k].y * p[s][k].y));
         const float2 dx = sub2(p[s][k], y[k]);
         acc[PT_IP] += fmaf(gr[k].x, dx.x, gr[k].y * dx.y);
@@ -475,7 +480,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
-template <bool TV>
+template <bool TV, bool MP>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   static_assert(NT <= 1024, "");
   extern __shared__ float4 dyn[];  // Bands, then (PF) [2][3][SR][NT] double-buffered prefetch slots
@@ -489,15 +494,15 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   };
   int work = next_from(blockIdx.x);
   if (work < 0) return;
-  if (PF && a.t0 == 0) prefetch_tile(a, pre, work);
+  if (PF && (!MP || a.t0 == 0)) prefetch_tile(a, pre, work);
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nxt = next_from(work + gridDim.x);
     const TileGeom tg = tile_geom(a, work % a.tiles_per_plane);
-    const bool edge = tg.rj0 == 0 || tg.rj0 + RW == a.nx;
+    const bool edge = tg.rj0 == 0 || tg.rj0 + RW == a.nx || tg.ri0 == 0 || tg.ri0 + RH == a.ny;
     if (edge)
-      prox_tile<TV, true>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+      prox_tile<TV, true, MP>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
     else
-      prox_tile<TV, false>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+      prox_tile<TV, false, MP>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
     work = nxt;
   }
 }
@@ -549,14 +554,18 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
   const long long total = (long long)a.tiles_per_plane * a.nplanes;
   const int grid = (int)std::min<long long>(total, nsm);
   if (grid <= 0) return cudaSuccess;
-  cudaError_t e;
-  if (a.tau_tv > 0.f) {
-    if ((e = cudaFuncSetAttribute(k_prox_strip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k_prox_strip<true><<<grid, NT, smem, s>>>(a);
-  } else {
-    if ((e = cudaFuncSetAttribute(k_prox_strip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    k_prox_strip<false><<<grid, NT, smem, s>>>(a);
-  }
+  cudaError_t e = cudaSuccess;
+  auto launch = [&](auto kern) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return;
+    kern<<<grid, NT, smem, s>>>(a);
+  };
+  if (a.tau_tv > 0.f && a.pass_len)
+    launch(k_prox_strip<true, true>);
+  else if (a.tau_tv > 0.f)
+    launch(k_prox_strip<true, false>);
+  else
+    launch(k_prox_strip<false, false>);  // no TV: no FGP passes
+  if (e) return e;
   return cudaGetLastError();
 }
 
