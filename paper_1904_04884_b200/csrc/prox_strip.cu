@@ -44,7 +44,7 @@ constexpr int NT = 32 * NW;
 // so the read needs no select; plane-edge regions (EDGE) apply the exact rule.
 struct Bands {
   float4 top[2][NW + 1][RW / 2];  // [buf][band][lane]: row-0 values (2 columns) -> down neighbour of the band above
-  float4 bot[NW + 1][RW / 2];     // row-(SR-1) values -> up neighbour of the band below
+  float4 bot[2][NW + 1][RW / 2];  // row-(SR-1) values (FGP sweep: X) -> up neighbour of the band below
 };
 
 HD float4 f4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
@@ -74,21 +74,38 @@ struct TileGeom {
   int i0, i1, j0, j1, ri0, rj0;
 };
 
-HD TileGeom tile_geom(const ProxArgs& a, int tile) {
-  TileGeom t;
-  const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+// n / d for 0 <= n < 2^24 via a host-side reciprocal (one correction step)
+HD int fdiv(int n, int d, float rcp) {
+  int q = __float2int_rz((float)n * rcp);
+  const int r = n - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+// Everything a region needs from its work index, computed once per region.
+struct Work {
+  int plane = -1;
+  TileGeom tg;
+  long long g0;  // this thread's first element (row 0 of its band, column pair)
+  bool edge;     // region touches a plane edge
+};
+
+HD Work work_geom(const ProxArgs& a, int work) {
+  Work wk;
+  wk.plane = fdiv(work, a.tiles_per_plane, a.rcp_tpp);
+  const int tile = work - wk.plane * a.tiles_per_plane;
+  const int ty = fdiv(tile, a.tiles_x, a.rcp_tx), tx = tile - ty * a.tiles_x;
+  TileGeom& t = wk.tg;
   t.i0 = ty * a.tile;
   t.j0 = tx * a.tile;
   t.i1 = min(a.ny, t.i0 + a.tile);
   t.j1 = min(a.nx, t.j0 + a.tile);
   t.ri0 = min(max(t.i0 - a.halo, 0), a.ny - RH);  // region clamped into the plane
   t.rj0 = min(max(t.j0 - a.halo, 0), a.nx - RW);
-  return t;
-}
-
-HD long long strip_base(const ProxArgs& a, int plane, const TileGeom& t) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return (long long)plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
+  wk.g0 = (long long)wk.plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
+  wk.edge = t.rj0 == 0 || t.rj0 + RW == a.nx || t.ri0 == 0 || t.ri0 + RH == a.ny;
+  return wk;
 }
 
 // per-thread prefetch slots: pre[(arr * SR + s) * NT + tid], arr = 0 x, 1 x_prev, 2 grad
@@ -96,15 +113,13 @@ HD void cp_async16(float4* smem_dst, const float2* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
-HD void prefetch_tile(const ProxArgs& a, float4* pre, int work) {
-  const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
-  const long long g0 = strip_base(a, plane, tile_geom(a, tile));
+HD void prefetch_tile(const ProxArgs& a, float4* pre, const Work& wk) {
+  const float2 *x = a.x + wk.g0, *xp = a.xp + wk.g0, *gr = a.grad + wk.g0;
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
-    const long long g = g0 + (long long)s * a.nx;
-    cp_async16(pre + (0 * SR + s) * NT + threadIdx.x, a.x + g);
-    if (a.beta != 0.f) cp_async16(pre + (1 * SR + s) * NT + threadIdx.x, a.xp + g);
-    if (a.grad) cp_async16(pre + (2 * SR + s) * NT + threadIdx.x, a.grad + g);
+    cp_async16(pre + (0 * SR + s) * NT + threadIdx.x, x + s * a.nx);
+    if (a.beta != 0.f) cp_async16(pre + (1 * SR + s) * NT + threadIdx.x, xp + s * a.nx);
+    if (a.grad) cp_async16(pre + (2 * SR + s) * NT + threadIdx.x, gr + s * a.nx);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -117,12 +132,12 @@ HD void prefetch_tile(const ProxArgs& a, float4* pre, int work) {
 // prefetch through shared memory only when the smem budget allows the double buffer
 constexpr bool PF = (SR >= 4);
 
-template <bool TV, bool EDGE, bool MP>
+template <bool TV, bool EDGE, int PH>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, float4* pre_next, int work,
-                                          int next_work) {
-  const int plane = work / a.tiles_per_plane, tile = work - plane * a.tiles_per_plane;
+                                          const Work& wk, const Work& nxt) {
+  const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
-  const TileGeom tg = tile_geom(a, tile);
+  const TileGeom& tg = wk.tg;
   const int i0 = tg.i0, i1 = tg.i1, j0 = tg.j0, j1 = tg.j1, ri0 = tg.ri0, rj0 = tg.rj0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool lane0 = lane == 0, lane31 = lane == 31;
@@ -138,12 +153,13 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     for (int k = 0; k < 2; ++k)
       if (rowInt && gj + k >= j0 && gj + k < j1) mInt |= 1u << (2 * s + k);
   }
-  const long long g0 = strip_base(a, plane, tg);
+  const long long g0 = wk.g0;
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
-  // MP: multi-pass launch (compile-time, so the single-pass kernel carries no pass state)
-  const bool first = !MP || a.t0 == 0, last = !MP || a.t1 >= a.inner;
-  const int pass = MP ? a.t0 / a.pass_len : 0;
+  // PH: pass kind of a multi-pass FGP (compile-time, so no kernel carries the
+  // state handling it does not use): 0 single pass, 1 first, 2 middle, 3 last
+  constexpr bool first = PH == 0 || PH == 1, last = PH == 0 || PH == 3;
+  const int pass = PH ? a.t0 / a.pass_len : 0;
   // state halves alternate by pass parity so a pass never overwrites what
   // neighbouring regions of the same launch still read as their halo
   const float4* s_in = a.sbuf + ((pass - 1) & 1) * a.sstride;
@@ -188,7 +204,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
     // the slots are free again (each thread only reads its own): overlap the
     // next region's HBM reads with this region's FGP iterations
-    if (PF && next_work >= 0) prefetch_tile(a, pre_next, next_work);  // (first pass only)
+    if (PF && nxt.plane >= 0) prefetch_tile(a, pre_next, nxt);  // (first pass only)
   }
 
   // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
@@ -210,9 +226,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     if (EDGE && lane31) r = make_float2(0.f, 0.f);
     return r;
   };
-  auto above_of = [&](int k, float2 self) -> float2 {
+  auto above_of = [&](int buf, int k, float2 self) -> float2 {
     if (EDGE && w == 0) return self;  // region top row: zero y-difference
-    const float4 b4 = sm.bot[w][lane];
+    const float4 b4 = sm.bot[buf][w][lane];
     return k ? hi2(b4) : lo2(b4);
   };
   const float2 mtau = splat2(-a.tau_tv);
@@ -220,12 +236,21 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
 
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
+    // X = v - tau (rp + rq - rq_right) of the band's last row: the last-row u
+    // without its rp_down term.  The band below rebuilds that u from X and its
+    // own row-0 rp, so one barrier per FGP iteration suffices.
+    auto xlast = [&](float2& x0, float2& x1) {
+      const float2 rqr1 = right_of(rq[SR - 1][0]);
+      x0 = fma2(mtau, sub2(add2(rp[SR - 1][0], rq[SR - 1][0]), rq[SR - 1][1]), v[SR - 1][0]);
+      x1 = fma2(mtau, sub2(add2(rp[SR - 1][1], rq[SR - 1][1]), rqr1), v[SR - 1][1]);
+    };
+    float2 xl0, xl1;
     if (first) {
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
-    sm.bot[w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
+    sm.bot[1][w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     __syncthreads();
     {
-      float2 up0 = above_of(0, v[0][0]), up1 = above_of(1, v[0][1]);
+      float2 up0 = above_of(1, 0, v[0][0]), up1 = above_of(1, 1, v[0][1]);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         float2 gx0, gx1;
@@ -254,40 +279,40 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         q[s][1] = rq[s][1] = qn1;
       }
     }
-    sm.top[0][w][lane] = f4(rp[0][0], rp[0][1]);
-    __syncthreads();
-    } else {
-      sm.top[(a.t0 - 1) & 1][w][lane] = f4(rp[0][0], rp[0][1]);  // the buffer the first sweep reads
+    }
+    // publish for the first sweep (iteration t reads buffer (t-1)&1, writes t&1)
+    {
+      const int b0 = first ? 0 : (a.t0 - 1) & 1;
+      xlast(xl0, xl1);
+      sm.top[b0][w][lane] = f4(rp[0][0], rp[0][1]);
+      sm.bot[b0][w + 1][lane] = f4(xl0, xl1);
       __syncthreads();
     }
     // ---- iterations max(t0,1)..t1-1: one fused sweep down the band per iteration ----
+    const float2 ptau = splat2(a.tau_tv);
 #pragma unroll 2
     for (int t = first ? 1 : a.t0; t < a.t1; ++t) {
-      const int b = (t - 1) & 1;  // buffer holding this iteration's band-top rp
+      const int b = (t - 1) & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
-      // u(s, k) = v - tau (rp + rq - rp_down - rq_right)
-      auto urow = [&](int s, float2 rpd0, float2 rpd1, float2& u0, float2& u1) {
-        const float2 rqr1 = right_of(rq[s][0]);
-        u0 = fma2(mtau, sub2(sub2(add2(rp[s][0], rq[s][0]), rpd0), rq[s][1]), v[s][0]);
-        u1 = fma2(mtau, sub2(sub2(add2(rp[s][1], rq[s][1]), rpd1), rqr1), v[s][1]);
-      };
-      // pre-pass: the band's last row, needed by the band below before its sweep
-      float2 ul0, ul1;
+      const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      // u of the row above the band: X of the band above + tau * my row-0 rp
+      float2 up0, up1;
       {
-        const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-        urow(SR - 1, lo2(d4), hi2(d4), ul0, ul1);
+        const float4 x4 = sm.bot[b][w][lane];
+        up0 = fma2(ptau, rp[0][0], lo2(x4));
+        up1 = fma2(ptau, rp[0][1], hi2(x4));
       }
-      sm.bot[w + 1][lane] = f4(ul0, ul1);
-      __syncthreads();
-      float2 up0 = above_of(0, make_float2(0.f, 0.f)), up1 = above_of(1, make_float2(0.f, 0.f));
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         float2 u0, u1;
         if (s == SR - 1) {
-          u0 = ul0;
-          u1 = ul1;
+          u0 = fma2(ptau, lo2(d4), xl0);
+          u1 = fma2(ptau, hi2(d4), xl1);
         } else {
-          urow(s, rp[s + 1][0], rp[s + 1][1], u0, u1);
+          // u(s, k) = v - tau (rp + rq - rp_down - rq_right)
+          const float2 rqr1 = right_of(rq[s][0]);
+          u0 = fma2(mtau, sub2(sub2(add2(rp[s][0], rq[s][0]), rp[s + 1][0]), rq[s][1]), v[s][0]);
+          u1 = fma2(mtau, sub2(sub2(add2(rp[s][1], rq[s][1]), rp[s + 1][1]), rqr1), v[s][1]);
         }
         if (EDGE && s == 0 && w == 0) {  // region top row: zero y-difference
           up0 = u0;
@@ -311,7 +336,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         p[s][1] = pn1;
         q[s][1] = qn1;
       }
-      sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffer: slower warps may read b
+      xlast(xl0, xl1);
+      sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
+      sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
       __syncthreads();
     }
     if (!last) {
@@ -365,11 +392,11 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         rp[s][1] = fma2(mtau, sub2(sub2(add2(p[s][1], q[s][1]), pd1), qr1), v[s][1]);
       }
     }
-    sm.bot[w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
+    sm.bot[0][w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
-      float2 up0 = above_of(0, rp[0][0]), up1 = above_of(1, rp[0][1]);
+      float2 up0 = above_of(0, 0, rp[0][0]), up1 = above_of(0, 1, rp[0][1]);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         float2 gx0, gx1;
@@ -415,10 +442,10 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       p[s][k] = make_float2(wr * gsc, wi * gsc);
     }
   }
-  sm.bot[w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+  sm.bot[0][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
   __syncthreads();
   {
-    float2 up0 = above_of(0, p[0][0]), up1 = above_of(1, p[0][1]);
+    float2 up0 = above_of(0, 0, p[0][0]), up1 = above_of(0, 1, p[0][1]);
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta);
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
@@ -460,13 +487,30 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
   }
   // fp32 warp sums (32 terms each), then fp64 across the 16 warps
+  // Transposed butterfly: each xor step halves the values a lane carries
+  // (it keeps one half and receives its partner's copy of it), so 8 slots
+  // cost 4+2+1+2 shuffles instead of 8x5; lane l ends with slot (l >> 2) & 7.
+  static_assert(kProxParts <= 8, "");
   __shared__ float wsum[NW][kProxParts];
+  {
+    float r8[8];
 #pragma unroll
-  for (int i = 0; i < kProxParts; ++i) {
-    float x = acc[i];
+    for (int i = 0; i < 8; ++i) r8[i] = i < kProxParts ? acc[i] : 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if (lane == 0) wsum[w][i] = x;
+    for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
+      const bool hi = lane & o;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const float send = hi ? r8[i] : r8[i + h];
+        const float keep = hi ? r8[i + h] : r8[i];
+        r8[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    float x = r8[0];
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    const int slot = (lane >> 2) & 7;
+    if ((lane & 3) == 0 && slot < kProxParts) wsum[w][slot] = x;
   }
   __syncthreads();
   if (threadIdx.x < kProxParts) {
@@ -480,7 +524,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
-template <bool TV, bool MP>
+template <bool TV, int PH>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   static_assert(NT <= 1024, "");
   extern __shared__ float4 dyn[];  // Bands, then (PF) [2][3][SR][NT] double-buffered prefetch slots
@@ -494,16 +538,18 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   };
   int work = next_from(blockIdx.x);
   if (work < 0) return;
-  if (PF && (!MP || a.t0 == 0)) prefetch_tile(a, pre, work);
+  Work cur = work_geom(a, work);
+  if (PF && (PH <= 1)) prefetch_tile(a, pre, cur);
   for (int buf = 0; work >= 0; buf ^= 1) {
-    const int nxt = next_from(work + gridDim.x);
-    const TileGeom tg = tile_geom(a, work % a.tiles_per_plane);
-    const bool edge = tg.rj0 == 0 || tg.rj0 + RW == a.nx || tg.ri0 == 0 || tg.ri0 + RH == a.ny;
-    if (edge)
-      prox_tile<TV, true, MP>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
+    const int nw = next_from(work + gridDim.x);
+    Work nxt;
+    if (nw >= 0) nxt = work_geom(a, nw);
+    if (cur.edge)
+      prox_tile<TV, true, PH>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, cur, nxt);
     else
-      prox_tile<TV, false, MP>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, nxt);
-    work = nxt;
+      prox_tile<TV, false, PH>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, cur, nxt);
+    work = nw;
+    cur = nxt;
   }
 }
 
@@ -541,6 +587,8 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.t1 = inner;
   a.tiles_x = (nx + a.tile - 1) / a.tile;
   a.tiles_per_plane = a.tiles_x * ((ny + a.tile - 1) / a.tile);
+  a.rcp_tx = 1.f / (float)a.tiles_x;
+  a.rcp_tpp = 1.f / (float)a.tiles_per_plane;
 }
 
 cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
@@ -559,12 +607,18 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return;
     kern<<<grid, NT, smem, s>>>(a);
   };
-  if (a.tau_tv > 0.f && a.pass_len)
-    launch(k_prox_strip<true, true>);
-  else if (a.tau_tv > 0.f)
-    launch(k_prox_strip<true, false>);
-  else
-    launch(k_prox_strip<false, false>);  // no TV: no FGP passes
+  if (a.tau_tv > 0.f && a.pass_len) {
+    if (a.t0 == 0)
+      launch(k_prox_strip<true, 1>);
+    else if (a.t1 >= a.inner)
+      launch(k_prox_strip<true, 3>);
+    else
+      launch(k_prox_strip<true, 2>);
+  } else if (a.tau_tv > 0.f) {
+    launch(k_prox_strip<true, 0>);
+  } else {
+    launch(k_prox_strip<false, 0>);  // no TV: no FGP passes
+  }
   if (e) return e;
   return cudaGetLastError();
 }
