@@ -44,6 +44,7 @@ struct ProxArgs {
   // multi-pass FGP (strip kernel, large T): this launch runs iterations [t0, t1);
   // the dual state crosses launches through HBM (interior pixels written,
   // region + halo read back by the next pass)
+  int tile_h = 0;                   // strip kernel: tile height (tile = width)
   float rcp_tx = 0.f, rcp_tpp = 0.f;  // strip kernel: 1/tiles_x, 1/tiles_per_plane (fast division)
   int t0 = 0, t1 = 0, pass_len = 0;  // pass_len 0: single pass
   float2* vbuf = nullptr;            // v = y - step grad (first pass writes)

@@ -21,7 +21,11 @@
 // Loads/stores are 16-byte (two complex64) per lane, 512 B per warp per row.
 // The FGP A/B half-steps are fused into one sweep down the band per
 // iteration, and the (re, im) arithmetic is packed FADD2/FMUL2/FFMA2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -30,7 +34,10 @@ namespace holo {
 namespace {
 
 constexpr int RW = 64;  // region width: one warp, 2 columns per lane
-constexpr int RH = 64;  // region height
+#ifndef HOLO_PROX_RH
+#define HOLO_PROX_RH 64
+#endif
+constexpr int RH = HOLO_PROX_RH;  // region height
 #ifndef HOLO_PROX_SR
 #define HOLO_PROX_SR 4
 #endif
@@ -96,9 +103,9 @@ HD Work work_geom(const ProxArgs& a, int work) {
   const int tile = work - wk.plane * a.tiles_per_plane;
   const int ty = fdiv(tile, a.tiles_x, a.rcp_tx), tx = tile - ty * a.tiles_x;
   TileGeom& t = wk.tg;
-  t.i0 = ty * a.tile;
+  t.i0 = ty * a.tile_h;
   t.j0 = tx * a.tile;
-  t.i1 = min(a.ny, t.i0 + a.tile);
+  t.i1 = min(a.ny, t.i0 + a.tile_h);
   t.j1 = min(a.nx, t.j0 + a.tile);
   t.ri0 = min(max(t.i0 - a.halo, 0), a.ny - RH);  // region clamped into the plane
   t.rj0 = min(max(t.j0 - a.halo, 0), a.nx - RW);
@@ -108,33 +115,60 @@ HD Work work_geom(const ProxArgs& a, int work) {
   return wk;
 }
 
-// per-thread prefetch slots: pre[(arr * SR + s) * NT + tid], arr = 0 x, 1 x_prev, 2 grad
-HD void cp_async16(float4* smem_dst, const float2* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+// Region inputs are staged by TMA: one elected thread loads the 64x64
+// complex box of x, x_prev and grad (32 KB each, row-major [row][2*col]
+// floats) into a double-buffered slot with one 2D tensor copy per array,
+// completing on an mbarrier, so the 512 threads issue no load instructions
+// and the next region's box streams in while this one iterates.
+constexpr int kSlotF4 = RH * RW / 2;  // float4 per array per slot
+constexpr int kSlotArrays = 3;        // x, x_prev, grad
+constexpr unsigned kArrayBytes = kSlotF4 * 16;
+
+struct TmaMaps {
+  CUtensorMap m[kSlotArrays];
+};
+
+HD unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+HD void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-HD void prefetch_tile(const ProxArgs& a, float4* pre, const Work& wk) {
-  const float2 *x = a.x + wk.g0, *xp = a.xp + wk.g0, *gr = a.grad + wk.g0;
+HD void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+HD void tma_region(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t* bar, const Work& wk) {
+  const int c0 = 2 * wk.tg.rj0, c1 = wk.plane * a.ny + wk.tg.ri0;
+  const bool use[kSlotArrays] = {true, a.beta != 0.f, a.grad != nullptr};
+  unsigned bytes = 0;
 #pragma unroll
-  for (int s = 0; s < SR; ++s) {
-    cp_async16(pre + (0 * SR + s) * NT + threadIdx.x, x + s * a.nx);
-    if (a.beta != 0.f) cp_async16(pre + (1 * SR + s) * NT + threadIdx.x, xp + s * a.nx);
-    if (a.grad) cp_async16(pre + (2 * SR + s) * NT + threadIdx.x, gr + s * a.nx);
+  for (int k = 0; k < kSlotArrays; ++k) bytes += use[k] ? kArrayBytes : 0u;
+  // the slot was last read through the generic proxy (behind a CTA barrier)
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+#pragma unroll
+  for (int k = 0; k < kSlotArrays; ++k) {
+    if (!use[k]) continue;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(slot + k * kSlotF4)),
+        "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
   }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-// One 64x64 region.  Inputs come from this thread's prefetch slots; the
-// prefetch of `next_work` (if >= 0) is issued as soon as the slots are read.
+// One region.  `pre` is its staged input slot (first / single pass) or null
+// (later passes of a multi-pass FGP read HBM directly).
 // EDGE: the region touches a plane edge, so its outer rows/columns need the
 // exact replicated-edge rule; otherwise they are garbage zone and the
 // lane-0 / lane-31 / band-0 / band-(NW-1) selects are skipped.
-// prefetch through shared memory only when the smem budget allows the double buffer
-constexpr bool PF = (SR >= 4);
-
 template <bool TV, bool EDGE, int PH>
-__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, float4* pre_next, int work,
-                                          const Work& wk, const Work& nxt) {
+__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, int work, const Work& wk) {
   const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
   const TileGeom& tg = wk.tg;
@@ -154,6 +188,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       if (rowInt && gj + k >= j0 && gj + k < j1) mInt |= 1u << (2 * s + k);
   }
   const long long g0 = wk.g0;
+  // this thread's float4 (2 columns) of row s of array k in the staged slot
+  auto slot = [&](int k, int s) { return pre[k * kSlotF4 + (r0 + s) * (RW / 2) + lane]; };
+  constexpr bool staged = PH <= 1;
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
   // PH: pass kind of a multi-pass FGP (compile-time, so no kernel carries the
@@ -182,19 +219,17 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
   } else {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
-    if (PF) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // my slots for this tile have landed
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
-      const long long g = g0 + (long long)s * a.nx;
-      const float4 y = PF ? pre[(0 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.x + g);
+      const float4 y = slot(0, s);
       float2 y0 = lo2(y), y1 = hi2(y);
       if (a.beta != 0.f) {
-        const float4 o = PF ? pre[(1 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.xp + g);
+        const float4 o = slot(1, s);
         y0 = fma2(cb, y0, mul2(cm, lo2(o)));
         y1 = fma2(cb, y1, mul2(cm, hi2(o)));
       }
       if (a.grad) {
-        float4 gg = PF ? pre[(2 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.grad + g);
+        float4 gg = slot(2, s);
         if (a.real_mode) gg.y = gg.w = 0.f;  // real engine: Re(grad) only
         y0 = fma2(cs, lo2(gg), y0);
         y1 = fma2(cs, hi2(gg), y1);
@@ -202,9 +237,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       v[s][0] = y0;
       v[s][1] = y1;
     }
-    // the slots are free again (each thread only reads its own): overlap the
-    // next region's HBM reads with this region's FGP iterations
-    if (PF && nxt.plane >= 0) prefetch_tile(a, pre_next, nxt);  // (first pass only)
   }
 
   // per-thread partial sums over its 8 pixels (fp32), promoted to fp64 at the end
@@ -370,8 +402,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
           a.tvv[(long long)work * 2 + threadIdx.x] = t;
         }
       }
-      __syncthreads();  // band buffers are reused by the next region
-      return;
+      return;  // every band read of this region precedes the last sweep's barrier
     }
     if (!first && threadIdx.x == 0) {  // TV(v) of this tile from the first pass
       acc[PT_G_R] += a.tvv[(long long)work * 2];
@@ -457,15 +488,15 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       const uint32_t rowbits = (mInt >> (2 * s)) & 3u;
       if (!rowbits) continue;
       const long long g = g0 + (long long)s * a.nx;
-      const float4 y4 = PF ? pre[(0 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.x + g);
+      const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
       float2 y[2] = {lo2(y4), hi2(y4)};
       if (a.beta != 0.f) {
-        const float4 o = PF ? pre[(1 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.xp + g);
+        const float4 o = staged ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
         y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
         y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
       }
       float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.grad) gr4 = PF ? pre[(2 * SR + s) * NT + threadIdx.x] : *reinterpret_cast<const float4*>(a.grad + g);
+      if (a.grad) gr4 = staged ? slot(2, s) : *reinterpret_cast<const float4*>(a.grad + g);
       if (a.real_mode) gr4.y = gr4.w = 0.f;
       const float2 gr[2] = {lo2(gr4), hi2(gr4)};
 #pragma unroll
@@ -513,23 +544,29 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     if ((lane & 3) == 0 && slot < kProxParts) wsum[w][slot] = x;
   }
   __syncthreads();
-  if (threadIdx.x < kProxParts) {
-    double t = 0.0;
+  // fp64 across the warps: 16 lanes per part (parts 2w', 2w'+1 in warp w')
+  static_assert(NW <= 16 && kProxParts % 2 == 0, "");
+  if (threadIdx.x < 16 * kProxParts) {
+    const int part = threadIdx.x >> 4, k = threadIdx.x & 15;
+    double t = k < NW ? (double)wsum[k][part] : 0.0;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) t += (double)wsum[k][threadIdx.x];
-    a.part[((long long)plane * a.tiles_per_plane + tile) * kProxParts + threadIdx.x] = t;
+    for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (k == 0) a.part[((long long)plane * a.tiles_per_plane + tile) * kProxParts + part] = t;
   }
-  __syncthreads();  // band buffers and wsum are reused by the next region
+  // No trailing barrier: every band / slot read of this region precedes the
+  // barrier above, and wsum is rewritten only after the next region's barriers.
 }
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
 template <bool TV, int PH>
-__global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
+__global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(NT <= 1024, "");
-  extern __shared__ float4 dyn[];  // Bands, then (PF) [2][3][SR][NT] double-buffered prefetch slots
+  extern __shared__ __align__(1024) float4 dyn[];  // Bands, then [2][3][RH][RW/2] float4 staged slots
   Bands& sm = *reinterpret_cast<Bands*>(dyn);
   float4* pre = dyn + sizeof(Bands) / sizeof(float4);
+  __shared__ uint64_t bars[2];
+  constexpr bool staged = PH <= 1;
   const int total = a.tiles_per_plane * a.nplanes;
   auto next_from = [&](int t) {
     if (a.force)
@@ -538,19 +575,52 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a) {
   };
   int work = next_from(blockIdx.x);
   if (work < 0) return;
-  Work cur = work_geom(a, work);
-  if (PF && (PH <= 1)) prefetch_tile(a, pre, cur);
+  const bool leader = threadIdx.x == 0;
+  if (staged && leader) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (staged && leader) tma_region(a, maps, pre, &bars[0], work_geom(a, work));
+  unsigned phase = 0;  // bit b: parity of slot b's next completion
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nw = next_from(work + gridDim.x);
-    Work nxt;
-    if (nw >= 0) nxt = work_geom(a, nw);
+    // the other slot was last read by the previous region, before its final barrier
+    if (staged && leader && nw >= 0)
+      tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], work_geom(a, nw));
+    const Work cur = work_geom(a, work);
+    const float4* slot = staged ? pre + buf * kSlotArrays * kSlotF4 : nullptr;
+    if (staged) {
+      mbar_wait(&bars[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    }
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, cur, nxt);
+      prox_tile<TV, true, PH>(a, sm, slot, work, cur);
     else
-      prox_tile<TV, false, PH>(a, sm, pre + buf * 3 * SR * NT, pre + (buf ^ 1) * 3 * SR * NT, work, cur, nxt);
+      prox_tile<TV, false, PH>(a, sm, slot, work, cur);
     work = nw;
-    cur = nxt;
   }
+}
+
+// 2D view [nplanes * ny rows][2 nx floats] of one complex64 stack, 64 x 128 boxes
+CUresult encode_map(CUtensorMap* m, const void* base, int ny_total, int nx) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return CUDA_ERROR_NOT_FOUND;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * nx, (cuuint64_t)ny_total};
+  const cuuint64_t strides[1] = {(cuuint64_t)2 * nx * sizeof(float)};
+  const cuuint32_t box[2] = {2 * RW, RH};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
 }  // namespace
@@ -582,11 +652,12 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   const int h_hi = tp ? h_lo : inner + (inner & 1);           // >= T, tile even
   a.halo = h_lo;
   a.tile = RW - h_lo - h_hi;
+  a.tile_h = RH - h_lo - h_hi;
   a.pass_len = tp;
   a.t0 = 0;
   a.t1 = inner;
   a.tiles_x = (nx + a.tile - 1) / a.tile;
-  a.tiles_per_plane = a.tiles_x * ((ny + a.tile - 1) / a.tile);
+  a.tiles_per_plane = a.tiles_x * ((ny + a.tile_h - 1) / a.tile_h);
   a.rcp_tx = 1.f / (float)a.tiles_x;
   a.rcp_tpp = 1.f / (float)a.tiles_per_plane;
 }
@@ -598,14 +669,22 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(Bands) + (PF ? sizeof(float4) * 2 * 3 * SR * NT : 0);
+  const size_t smem = sizeof(Bands) + sizeof(float4) * 2 * kSlotArrays * kSlotF4;
+  TmaMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (a.pass_len == 0 || a.t0 == 0) {  // staged passes
+    const int rows = a.nplanes * a.ny;
+    if (encode_map(&maps.m[0], a.x, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (a.beta != 0.f && encode_map(&maps.m[1], a.xp, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (a.grad && encode_map(&maps.m[2], a.grad, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   const long long total = (long long)a.tiles_per_plane * a.nplanes;
   const int grid = (int)std::min<long long>(total, nsm);
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   auto launch = [&](auto kern) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return;
-    kern<<<grid, NT, smem, s>>>(a);
+    kern<<<grid, NT, smem, s>>>(a, maps);
   };
   if (a.tau_tv > 0.f && a.pass_len) {
     if (a.t0 == 0)
