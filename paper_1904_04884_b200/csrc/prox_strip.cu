@@ -177,16 +177,17 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   const bool lane0 = lane == 0, lane31 = lane == 31;
   const int r0 = w * SR;
   const int gj = rj0 + 2 * lane;  // columns gj, gj+1
-  // interior bits: bit (2 s + k) for row s, column k
-  uint32_t mInt = 0;
+  // Interior pixels: rows are warp-uniform (bit s of rInt: whole rows of halo
+  // are skipped by uniform branches), and columns come in aligned pairs (tile
+  // and halo are even), so a lane's two columns are both in or both out: the
+  // statistics are accumulated unmasked and dropped per lane at the end.
+  uint32_t rInt = 0;
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
     const int gi = ri0 + r0 + s;
-    const bool rowInt = gi >= i0 && gi < i1;
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (rowInt && gj + k >= j0 && gj + k < j1) mInt |= 1u << (2 * s + k);
+    if (gi >= i0 && gi < i1) rInt |= 1u << s;
   }
+  const bool cInt = gj >= j0 && gj < j1;
   const long long g0 = wk.g0;
   // this thread's float4 (2 columns) of row s of array k in the staged slot
   auto slot = [&](int k, int s) { return pre[k * kSlotF4 + (r0 + s) * (RW / 2) + lane]; };
@@ -291,13 +292,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         up0 = v[s][0];
         up1 = v[s][1];
         // guard: G = tau TV(w) + |w - v|^2 / 2 - tau TV(v) per part, here the -tau TV(v) term
-        if (mInt & (1u << (2 * s))) {
-          const float2 nv = norm_pair(gy0, gx0);
-          acc[PT_G_R] = fmaf(-ttv, nv.x, acc[PT_G_R]);
-          acc[PT_G_I] = fmaf(-ttv, nv.y, acc[PT_G_I]);
-        }
-        if (mInt & (2u << (2 * s))) {
-          const float2 nv = norm_pair(gy1, gx1);
+        if (rInt & (1u << s)) {
+          const float2 nv = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
           acc[PT_G_R] = fmaf(-ttv, nv.x, acc[PT_G_R]);
           acc[PT_G_I] = fmaf(-ttv, nv.y, acc[PT_G_I]);
         }
@@ -378,15 +374,16 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         const long long g = g0 + (long long)s * a.nx;
+        if (!(rInt & (1u << s)) || !cInt) continue;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          if (!(mInt & (1u << (2 * s + k)))) continue;
           a.sbuf[(pass & 1) * a.sstride + g + k] = f4(p[s][k], q[s][k]);
           a.rbuf[(pass & 1) * a.sstride + g + k] = f4(rp[s][k], rq[s][k]);
-          if (first) a.vbuf[g + k] = v[s][k];
         }
+        if (first) *reinterpret_cast<float4*>(a.vbuf + g) = f4(v[s][0], v[s][1]);
       }
       if (first) {  // TV(v) guard partials of this tile, consumed by the last pass
+        if (!cInt) acc[PT_G_R] = acc[PT_G_I] = 0.f;
         __shared__ float tsum[NW][2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -403,10 +400,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         }
       }
       return;  // every band read of this region precedes the last sweep's barrier
-    }
-    if (!first && threadIdx.x == 0) {  // TV(v) of this tile from the first pass
-      acc[PT_G_R] += a.tvv[(long long)work * 2];
-      acc[PT_G_I] += a.tvv[(long long)work * 2 + 1];
     }
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
     const int bf = a.inner & 1;  // not read by the last sweep
@@ -435,14 +428,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         const float2 gy0 = sub2(rp[s][0], up0), gy1 = sub2(rp[s][1], up1);
         up0 = rp[s][0];
         up1 = rp[s][1];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          if (mInt & (1u << (2 * s + k))) {
-            const float2 nw = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
-            const float2 dv = sub2(rp[s][k], v[s][k]);
-            acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f * dv.x, dv.x, acc[PT_G_R]));
-            acc[PT_G_I] = fmaf(ttv, nw.y, fmaf(0.5f * dv.y, dv.y, acc[PT_G_I]));
-          }
+        if (rInt & (1u << s)) {
+          const float2 nw = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
+          const float2 d0 = sub2(rp[s][0], v[s][0]), d1 = sub2(rp[s][1], v[s][1]);
+          const float2 dd = fma2(d0, d0, mul2(d1, d1));  // (re, im) |w - v|^2 of the pair
+          acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f, dd.x, acc[PT_G_R]));
+          acc[PT_G_I] = fmaf(ttv, nw.y, fmaf(0.5f, dd.y, acc[PT_G_I]));
         }
       }
     }
@@ -485,8 +476,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       const float2 gy0 = sub2(p[s][0], up0), gy1 = sub2(p[s][1], up1);
       up0 = p[s][0];
       up1 = p[s][1];
-      const uint32_t rowbits = (mInt >> (2 * s)) & 3u;
-      if (!rowbits) continue;
+      if (!(rInt & (1u << s))) continue;
       const long long g = g0 + (long long)s * a.nx;
       const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
       float2 y[2] = {lo2(y4), hi2(y4)};
@@ -499,22 +489,20 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
       if (a.grad) gr4 = staged ? slot(2, s) : *reinterpret_cast<const float4*>(a.grad + g);
       if (a.real_mode) gr4.y = gr4.w = 0.f;
       const float2 gr[2] = {lo2(gr4), hi2(gr4)};
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (!(rowbits & (1u << k))) continue;
-        const float2 nx2 = norm_pair(k ? gy1 : gy0, k ? gx1 : gx0);
+      {
+        const float2 nx2 = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
         acc[PT_TVX] += nx2.x + nx2.y;
-        acc[PT_L1] += sqrt_a(fmaf(p[s][k].x, p[s][k].x, p[s][k].y * p[s][k].y));
-        const float2 dx = sub2(p[s][k], y[k]);
-        acc[PT_IP] += fmaf(gr[k].x, dx.x, gr[k].y * dx.y);
-        acc[PT_DX2] += fmaf(dx.x, dx.x, dx.y * dx.y);
+        // |x| of both columns: (re^2 + im^2) packed as (col 0, col 1)
+        const float2 re = make_float2(p[s][0].x, p[s][1].x), im = make_float2(p[s][0].y, p[s][1].y);
+        const float2 m2 = fma2(re, re, mul2(im, im));
+        acc[PT_L1] += sqrt_a(m2.x) + sqrt_a(m2.y);
+        const float2 dx0 = sub2(p[s][0], y[0]), dx1 = sub2(p[s][1], y[1]);
+        const float2 ip = fma2(gr[0], dx0, mul2(gr[1], dx1));       // (re, im) parts of <g, dx>
+        const float2 d2 = fma2(dx0, dx0, mul2(dx1, dx1));
+        acc[PT_IP] += ip.x + ip.y;
+        acc[PT_DX2] += d2.x + d2.y;
       }
-      if (rowbits == 3u) {
-        *reinterpret_cast<float4*>(a.xnew + g) = f4(p[s][0], p[s][1]);
-      } else {
-        if (rowbits & 1u) a.xnew[g] = p[s][0];
-        if (rowbits & 2u) a.xnew[g + 1] = p[s][1];
-      }
+      if (cInt) *reinterpret_cast<float4*>(a.xnew + g) = f4(p[s][0], p[s][1]);
     }
   }
   // fp32 warp sums (32 terms each), then fp64 across the 16 warps
@@ -522,6 +510,14 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
   // (it keeps one half and receives its partner's copy of it), so 8 slots
   // cost 4+2+1+2 shuffles instead of 8x5; lane l ends with slot (l >> 2) & 7.
   static_assert(kProxParts <= 8, "");
+  if (!cInt) {  // halo columns
+#pragma unroll
+    for (int i = 0; i < kProxParts; ++i) acc[i] = 0.f;
+  }
+  if (TV && !first && threadIdx.x == 0) {  // -tau TV(v) of this tile from the first pass
+    acc[PT_G_R] += a.tvv[(long long)work * 2];
+    acc[PT_G_I] += a.tvv[(long long)work * 2 + 1];
+  }
   __shared__ float wsum[NW][kProxParts];
   {
     float r8[8];
