@@ -124,6 +124,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def measured_traffic(kernel, voxels):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, scaled from
+    the committed ncu --set full capture of one launch (profiles/r01_traffic.json,
+    written by tools/ncu_traffic.py); None if that kernel was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            rec = json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+    return None if rec is None else rec["dram_bytes_per_voxel"] * voxels
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -310,6 +322,7 @@ def main():
     dom = max((k for k in prof if k in KERNEL_BYTES), key=lambda k: prof[k]["ms"])
     per_launch_s = prof[dom]["ms"] / 1e3 / max(prof[dom]["launches"], 1)
     achieved = KERNEL_BYTES[dom] * local_vox / per_launch_s / 1e9
+    traffic = measured_traffic(dom, local_vox)
     total_kernel_ms = sum(v["ms"] for v in prof.values())
     step_roof = value / world * BYTES_PER_VOXEL_ITER / 1e9
 
@@ -346,7 +359,7 @@ def main():
                                    f"{n_particles(cfg)} particles d=20um, lambda=({l1},{tv}), T={inner}",
                        "l2": "inputs larger than L2 (state 3 x 4.3 GB complex64)", "parallelism": f"z-shard x{world}"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_voxel": KERNEL_BYTES[dom]},
             "step_roofline": {"bytes_per_voxel_iter": BYTES_PER_VOXEL_ITER, "achieved": step_roof, "peak": hbm,
                               "frac": step_roof / hbm},
