@@ -874,25 +874,39 @@ cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, 
   return err ? err : cudaGetLastError();
 }
 
+#ifndef HOLO_ADJ_C
+#define HOLO_ADJ_C(N) ((N) >= 4096 ? 4 : 8)  // 16 measured slower at 1024
+#endif
+#ifndef HOLO_FWD_C
+#define HOLO_FWD_C(N) ((N) >= 1024 ? 8 : 4)
+#endif
+
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
     constexpr int E = DefaultE<N>::value;  // radix-32 columns measured slower (occupancy)
-    constexpr int C = N >= 4096 ? 4 : 8;
-    constexpr int NT = C * FftShape<N, E>::TPF;
-    const size_t smem = col_smem<N, C, E>(256);
-    dim3 grid(p.nx / C, nzl);
-    err = set_smem(k_adj_cols<N, C, E>, smem);
-    k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
-  COUNT_LAUNCH(1);
+    auto launch = [&](auto cc) {
+      constexpr int C = decltype(cc)::value;  // C x 8-byte row segments per warp load / store
+      constexpr int NT = C * FftShape<N, E>::TPF;
+      const size_t smem = col_smem<N, C, E>(256);
+      dim3 grid(p.nx / C, nzl);
+      err = set_smem(k_adj_cols<N, C, E>, smem);
+      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
+    };
+    constexpr int CW = HOLO_ADJ_C(N);
+    if (p.nx >= CW)
+      launch(std::integral_constant<int, CW>());
+    else
+      launch(std::integral_constant<int, 8>());  // nx >= 8 always
+    COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
   return err ? err : cudaGetLastError();
 }
 
 int fwd_groups(const Plan& p, int nzl) {
-  const int tiles = std::max(1, p.nx / 4);
+  const int tiles = std::max(1, p.nx / HOLO_FWD_C(p.ny));
   int g = (16 * 148 + tiles - 1) / tiles;  // ~8 waves of 2 CTAs/SM: small tail
   g = std::max(1, std::min(g, nzl));
   return std::min(g, 64);
@@ -904,7 +918,7 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
     constexpr int E = DefaultE<N>::value;  // acc[] + v[] per thread
-    constexpr int C = 4;  // 256-thread CTAs keep acc[] + v[] in registers
+    constexpr int C = HOLO_FWD_C(N);  // acc[] + v[] stay in registers at <= 128 per thread
     constexpr int NT = C * FftShape<N, E>::TPF;
     const size_t smem = col_smem<N, C, E>(256);
     dim3 grid(p.nx / C, groups);

@@ -162,13 +162,27 @@ HD void tma_region(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_
   }
 }
 
+// Band-slot split barrier: mbarriers with one arrival per warp (lane 0, after
+// __syncwarp orders the warp's slot writes; release), waited on by every
+// thread (acquire).  bph holds each barrier's next completion parity.
+HD void band_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+HD void band_wait(uint64_t* bars, int i, unsigned& bph) {
+  mbar_wait(&bars[i], (bph >> i) & 1u);
+  bph ^= 1u << i;
+}
+
 // One region.  `pre` is its staged input slot (first / single pass) or null
 // (later passes of a multi-pass FGP read HBM directly).
 // EDGE: the region touches a plane edge, so its outer rows/columns need the
 // exact replicated-edge rule; otherwise they are garbage zone and the
 // lane-0 / lane-31 / band-0 / band-(NW-1) selects are skipped.
 template <bool TV, bool EDGE, int PH>
-__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const float4* pre, int work, const Work& wk) {
+__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t* bbar, unsigned& bph, const float4* pre,
+                                          int work, const Work& wk) {
   const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
   const TileGeom& tg = wk.tg;
@@ -309,48 +323,27 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
     }
     }
     // publish for the first sweep (iteration t reads buffer (t-1)&1, writes t&1)
+    int lastbuf = first ? 0 : (a.t0 - 1) & 1;
     {
-      const int b0 = first ? 0 : (a.t0 - 1) & 1;
       xlast(xl0, xl1);
-      sm.top[b0][w][lane] = f4(rp[0][0], rp[0][1]);
-      sm.bot[b0][w + 1][lane] = f4(xl0, xl1);
-      __syncthreads();
+      sm.top[lastbuf][w][lane] = f4(rp[0][0], rp[0][1]);
+      sm.bot[lastbuf][w + 1][lane] = f4(xl0, xl1);
+      band_arrive(&bbar[lastbuf]);
     }
     // ---- iterations max(t0,1)..t1-1: one fused sweep down the band per iteration ----
+    // Split barrier: rows 1..SR-2 only need this band's registers, so they are
+    // updated between the previous iteration's arrive and the wait for the
+    // neighbours' band data; rows 0 and SR-1 follow the wait.
     const float2 ptau = splat2(a.tau_tv);
 #pragma unroll 2
     for (int t = first ? 1 : a.t0; t < a.t1; ++t) {
       const int b = (t - 1) & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
-      const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-      // u of the row above the band: X of the band above + tau * my row-0 rp
-      float2 up0, up1;
-      {
-        const float4 x4 = sm.bot[b][w][lane];
-        up0 = fma2(ptau, rp[0][0], lo2(x4));
-        up1 = fma2(ptau, rp[0][1], hi2(x4));
-      }
-#pragma unroll
-      for (int s = 0; s < SR; ++s) {
-        float2 u0, u1;
-        if (s == SR - 1) {
-          u0 = fma2(ptau, lo2(d4), xl0);
-          u1 = fma2(ptau, hi2(d4), xl1);
-        } else {
-          // u(s, k) = v - tau (rp + rq - rp_down - rq_right)
-          const float2 rqr1 = right_of(rq[s][0]);
-          u0 = fma2(mtau, sub2(sub2(add2(rp[s][0], rq[s][0]), rp[s + 1][0]), rq[s][1]), v[s][0]);
-          u1 = fma2(mtau, sub2(sub2(add2(rp[s][1], rq[s][1]), rp[s + 1][1]), rqr1), v[s][1]);
-        }
-        if (EDGE && s == 0 && w == 0) {  // region top row: zero y-difference
-          up0 = u0;
-          up1 = u1;
-        }
+      // one row's dual update from its u, given the u of the row above
+      auto update = [&](int s, float2 u0, float2 u1, float2 up0, float2 up1) {
         float2 gx0, gx1;
         gx_row(u0, u1, gx0, gx1);
         const float2 gy0 = sub2(u0, up0), gy1 = sub2(u1, up1);
-        up0 = u0;
-        up1 = u1;
         float2 pn0 = fma2(lr2, gy0, rp[s][0]), qn0 = fma2(lr2, gx0, rq[s][0]);
         float2 pn1 = fma2(lr2, gy1, rp[s][1]), qn1 = fma2(lr2, gx1, rq[s][1]);
         project(pn0, qn0);
@@ -363,12 +356,39 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, const fl
         q[s][0] = qn0;
         p[s][1] = pn1;
         q[s][1] = qn1;
+      };
+      // u(s, k) = v - tau (rp + rq - rp_down - rq_right) for rows 0..SR-2 (own registers)
+      float2 u[SR - 1][2];
+#pragma unroll
+      for (int s = 0; s < SR - 1; ++s) {
+        const float2 rqr1 = right_of(rq[s][0]);
+        u[s][0] = fma2(mtau, sub2(sub2(add2(rp[s][0], rq[s][0]), rp[s + 1][0]), rq[s][1]), v[s][0]);
+        u[s][1] = fma2(mtau, sub2(sub2(add2(rp[s][1], rq[s][1]), rp[s + 1][1]), rqr1), v[s][1]);
       }
+      // the u of the row above row 0 uses row 0's rp before its update: keep it
+      const float2 r00 = rp[0][0], r01 = rp[0][1];
+#pragma unroll
+      for (int s = 1; s < SR - 1; ++s) update(s, u[s][0], u[s][1], u[s - 1][0], u[s - 1][1]);
+      band_wait(bbar, b, bph);
+      const float4 d4 = (!EDGE || w < NW - 1) ? sm.top[b][w + 1][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 x4 = sm.bot[b][w][lane];
+      {
+        // u of the row above the band: X of the band above + tau * my row-0 rp
+        float2 up0 = fma2(ptau, r00, lo2(x4)), up1 = fma2(ptau, r01, hi2(x4));
+        if (EDGE && w == 0) {  // region top row: zero y-difference
+          up0 = u[0][0];
+          up1 = u[0][1];
+        }
+        update(0, u[0][0], u[0][1], up0, up1);
+      }
+      update(SR - 1, fma2(ptau, lo2(d4), xl0), fma2(ptau, hi2(d4), xl1), u[SR - 2][0], u[SR - 2][1]);
       xlast(xl0, xl1);
       sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
       sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
-      __syncthreads();
+      band_arrive(&bbar[b ^ 1]);
+      lastbuf = b ^ 1;
     }
+    band_wait(bbar, lastbuf, bph);  // every band's last publication (and its reads of the other buffer) is done
     if (!last) {
       // hand the dual state (and v, once) of the interior pixels to the next pass
 #pragma unroll
@@ -561,7 +581,8 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   extern __shared__ __align__(1024) float4 dyn[];  // Bands, then [2][3][RH][RW/2] float4 staged slots
   Bands& sm = *reinterpret_cast<Bands*>(dyn);
   float4* pre = dyn + sizeof(Bands) / sizeof(float4);
-  __shared__ uint64_t bars[2];
+  __shared__ uint64_t bars[2];   // TMA slot completion
+  __shared__ uint64_t bbar[2];   // band-slot split barrier (one arrival per warp)
   constexpr bool staged = PH <= 1;
   const int total = a.tiles_per_plane * a.nplanes;
   auto next_from = [&](int t) {
@@ -572,14 +593,17 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   int work = next_from(blockIdx.x);
   if (work < 0) return;
   const bool leader = threadIdx.x == 0;
-  if (staged && leader) {
+  if (leader) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bbar[0], NW);
+    mbar_init(&bbar[1], NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (staged && leader) tma_region(a, maps, pre, &bars[0], work_geom(a, work));
   unsigned phase = 0;  // bit b: parity of slot b's next completion
+  unsigned bph = 0;    // bit b: parity of band barrier b's next completion
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nw = next_from(work + gridDim.x);
     // the other slot was last read by the previous region, before its final barrier
@@ -592,9 +616,9 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
       phase ^= 1u << buf;
     }
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, sm, slot, work, cur);
+      prox_tile<TV, true, PH>(a, sm, bbar, bph, slot, work, cur);
     else
-      prox_tile<TV, false, PH>(a, sm, slot, work, cur);
+      prox_tile<TV, false, PH>(a, sm, bbar, bph, slot, work, cur);
     work = nw;
   }
 }
