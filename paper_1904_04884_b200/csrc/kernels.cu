@@ -15,6 +15,9 @@
 //   solver.py:126-132 (gradient_chunks)          -> K6 + K2 + K3
 //   solver.py:309-318, prox.py:83-148            -> K4
 //   sparsevol.py:75-88 (from_dense)              -> K7
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -181,7 +184,8 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
 template <int N, int C, int E_>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const float2* __restrict__ R,
                                                                     float2* __restrict__ out, int nx, long long P,
-                                                                    int k0, const uint64_t* __restrict__ tab,
+                                                                    int k0, int nzl, int ppc,
+                                                                    const uint64_t* __restrict__ tab,
                                                                     const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
   using Sh = FftShape<N, E_>;
@@ -195,15 +199,27 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
-  const int k = blockIdx.y;
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
-  float2 v[E];
+  // R and the packed phase of this thread's column elements are the same for
+  // every plane: load them once (L2) and keep them in registers for the
+  // CTA's planes, so the plane loop issues no global loads.
+  float2 r[E];
+  uint64_t ph[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ));
-  fft_line<N, true, E_>(v, j, buf + c, C, tw);
-  float2* dst = out + (long long)k * P + p0;
+  for (int m = 0; m < E; ++m) {
+    r[m] = R[p0 + m * st];
+    ph[m] = tab[p0 + m * st];
+  }
+  const int kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
+  for (int k = kb; k < ke; ++k) {
+    float2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) dst[m * st] = v[m];
+    for (int m = 0; m < E; ++m) v[m] = cmul(r[m], cis_cycles(plane_phase(ph[m], k0 + k), circ));
+    fft_line<N, true, E_>(v, j, buf + c, C, tw);
+    float2* dst = out + (long long)k * P + p0;
+#pragma unroll
+    for (int m = 0; m < E; ++m) dst[m * st] = v[m];
+  }
 }
 
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
@@ -238,6 +254,91 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
     // transfer multiply-accumulate in chunks of 4: bounds the table loads in
     // flight (16 B each) so acc[] + v[] stay in registers
+#pragma unroll
+    for (int m0 = 0; m0 < E; m0 += 4) {
+#pragma unroll
+      for (int m = m0; m < m0 + 4 && m < E; ++m)
+        acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ)));
+      asm volatile("" ::: "memory");
+    }
+  }
+  float2* dst = Spart + (long long)blockIdx.y * P + p0;
+#pragma unroll
+  for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
+}
+
+// K5 with TMA staging (N <= 1024): one elected thread streams plane k+1's
+// C-column block (N rows x C complex) into the other half of a double-buffered
+// shared-memory stage with 2D tensor copies while the CTA transforms plane k,
+// so the column loads leave the critical path (the plain kernel waited on HBM
+// once per plane with only 16 warps per SM to hide it).
+template <int N, int C, int E_>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged(
+    const __grid_constant__ CUtensorMap in_map, float2* __restrict__ Spart, int nx, long long P, int ny, int nzl,
+    int ppg, int k0, const uint64_t* __restrict__ tab, const float4* __restrict__ twg,
+    const float2* __restrict__ circg) {
+  using Sh = FftShape<N, E_>;
+  constexpr int TPF = Sh::TPF, E = Sh::E;
+  constexpr int BOX_ROWS = N < 256 ? N : 256;
+  extern __shared__ __align__(128) float2 smem[];
+  float2* stage = smem;                             // [2][N][C]
+  float4* tw = reinterpret_cast<float4*>(smem + 2 * N * C);
+  float2* circ = smem + 2 * N * C + 2 * N;
+  float2* buf = smem + 2 * N * C + 2 * N + 256;
+  __shared__ uint64_t bars[2];
+  const int kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
+  const bool leader = threadIdx.x == 0;
+  auto issue = [&](int k, int b) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                 "r"((unsigned)(N * C * sizeof(float2)))
+                 : "memory");
+#pragma unroll
+    for (int r0 = 0; r0 < N; r0 += BOX_ROWS)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+              (unsigned)__cvta_generic_to_shared(stage + (size_t)b * N * C + (size_t)r0 * C)),
+          "l"(reinterpret_cast<uint64_t>(&in_map)), "r"(2 * (int)blockIdx.x * C), "r"(k * ny + r0), "r"(bar)
+          : "memory");
+  };
+  if (leader) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bars[b]))
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (leader && kb < ke) issue(kb, 0);
+  for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
+  __syncthreads();
+  const int c = threadIdx.x % C, j = threadIdx.x / C;
+  const int col = blockIdx.x * C + c;
+  float2 acc[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) acc[m] = czero();
+  const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
+  for (int k = kb; k < ke; ++k) {
+    const int b = (k - kb) & 1;
+    // the other stage was last read in the previous plane, before fft_line's barriers
+    if (leader && k + 1 < ke) issue(k + 1, b ^ 1);
+    {
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]), par = ((k - kb) >> 1) & 1;
+      unsigned done = 0;
+      do {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(par)
+            : "memory");
+      } while (!done);
+    }
+    float2 v[E];
+    const float2* src = stage + (size_t)b * N * C + c;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = src[(j + m * TPF) * C];
+    fft_line<N, false, E_>(v, j, buf + c, C, tw);
 #pragma unroll
     for (int m0 = 0; m0 < E; m0 += 4) {
 #pragma unroll
@@ -846,6 +947,28 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
   return err ? err : cudaGetLastError();
 }
 
+// 2D tiled tensor map over float32 rows (inner = floats per row, rows), box
+// box_inner x box_rows; nonzero on failure.  The driver entry point is looked
+// up at run time (no libcuda link dependency).
+int encode_tiled_2d(CUtensorMap* m, const void* base, long long inner, long long rows, int box_inner, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return 1;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)inner * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS;
+}
+
 template <int N, int C, int E>
 static size_t col_smem(int extra) {
   return sizeof(float2) * (2 * N + extra + (size_t)(N + N / E) * C);
@@ -874,12 +997,13 @@ cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, 
   return err ? err : cudaGetLastError();
 }
 
-#ifndef HOLO_ADJ_C
-#define HOLO_ADJ_C(N) ((N) >= 4096 ? 4 : 8)  // 16 measured slower at 1024
+#ifndef HOLO_ADJ_PPC
+#define HOLO_ADJ_PPC 64
 #endif
-#ifndef HOLO_FWD_C
+// 4 columns (256 threads) per CTA: with R / phase held in registers across the
+// CTA's planes (126 registers) two CTAs fit per SM (measured best at 1024^2)
+#define HOLO_ADJ_C(N) 4
 #define HOLO_FWD_C(N) ((N) >= 1024 ? 8 : 4)
-#endif
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
@@ -890,15 +1014,15 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
       constexpr int C = decltype(cc)::value;  // C x 8-byte row segments per warp load / store
       constexpr int NT = C * FftShape<N, E>::TPF;
       const size_t smem = col_smem<N, C, E>(256);
-      dim3 grid(p.nx / C, nzl);
+      // planes per CTA: >= ~8 waves of CTAs in the grid
+      const long long blocks = p.nx / C;
+      const int ppc = (int)std::max(1LL, std::min<long long>(HOLO_ADJ_PPC, blocks * nzl / (148LL * 8)));
+      dim3 grid(p.nx / C, (nzl + ppc - 1) / ppc);
       err = set_smem(k_adj_cols<N, C, E>, smem);
-      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
+      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()],
+                                                  p.circle);
     };
-    constexpr int CW = HOLO_ADJ_C(N);
-    if (p.nx >= CW)
-      launch(std::integral_constant<int, CW>());
-    else
-      launch(std::integral_constant<int, 8>());  // nx >= 8 always
+    launch(std::integral_constant<int, HOLO_ADJ_C(N)>());  // nx >= 8 always
     COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
@@ -920,11 +1044,23 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
     constexpr int E = DefaultE<N>::value;  // acc[] + v[] per thread
     constexpr int C = HOLO_FWD_C(N);  // acc[] + v[] stay in registers at <= 128 per thread
     constexpr int NT = C * FftShape<N, E>::TPF;
-    const size_t smem = col_smem<N, C, E>(256);
     dim3 grid(p.nx / C, groups);
-    err = set_smem(k_fwd_cols<N, C, E>, smem);
-    k_fwd_cols<N, C, E><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
-                                                p.circle);
+    if constexpr (N <= 1024) {
+      CUtensorMap map;
+      if (encode_tiled_2d(&map, in, 2 * p.nx, (long long)nzl * p.ny, 2 * C, N < 256 ? N : 256)) {
+        err = cudaErrorInvalidValue;
+        return;
+      }
+      const size_t smem = col_smem<N, C, E>(256) + sizeof(float2) * 2 * N * C;
+      err = set_smem(k_fwd_cols_staged<N, C, E>, smem);
+      k_fwd_cols_staged<N, C, E><<<grid, NT, smem, s>>>(map, Spart, p.nx, p.P, p.ny, nzl, ppg, k0, p.phase,
+                                                         p.tw_y[tw_slot<E>()], p.circle);
+    } else {
+      const size_t smem = col_smem<N, C, E>(256);
+      err = set_smem(k_fwd_cols<N, C, E>, smem);
+      k_fwd_cols<N, C, E><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
+                                                  p.circle);
+    }
   COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;

@@ -1,5 +1,6 @@
 // Host-side launch interface of the sm_100a kernels (kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -54,6 +55,8 @@ struct ProxArgs {
   float* tvv = nullptr;              // per-tile TV(v) partials [tile][2], first pass -> last pass
 };
 
+// 2D tiled TMA descriptor over float rows (kernels.cu); nonzero on failure
+int encode_tiled_2d(CUtensorMap* m, const void* base, long long inner, long long rows, int box_inner, int box_rows);
 bool plan_supported(int nx, int ny);
 long long launch_count();  // kernels launched by this library since load
 cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,
