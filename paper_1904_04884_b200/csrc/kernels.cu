@@ -180,6 +180,9 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
   for (int m = 0; m < E; ++m) out[base + m * st] = cscale(v[m], scale);
 }
 
+#ifndef HOLO_ADJ_RECUR
+#define HOLO_ADJ_RECUR 1
+#endif
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
 template <int N, int C, int E_>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const float2* __restrict__ R,
@@ -200,6 +203,33 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
+#if HOLO_ADJ_RECUR
+  // H_{k+1} = H_k * G with G = cis(2 pi dz q) per pixel: R H_k is carried from
+  // plane to plane by one complex multiply (the reference's TransferLadder
+  // recurrence, optics.py:146-169), exact cis() only at the CTA's first plane
+  // (<= HOLO_ADJ_PPC steps: < 4e-6 relative drift worst case).
+  const int kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
+  float2 r[E], g[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const uint64_t t = tab[p0 + m * st];
+    r[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(t, k0 + kb), circ));
+    g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+  }
+  for (int k = kb; k < ke; ++k) {
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      v[m] = r[m];
+      r[m] = cmul(r[m], g[m]);
+    }
+    fft_line<N, true, E_>(v, j, buf + c, C, tw);
+    float2* dst = out + (long long)k * P + p0;
+#pragma unroll
+    for (int m = 0; m < E; ++m) dst[m * st] = v[m];
+  }
+}
+#else
   // R and the packed phase of this thread's column elements are the same for
   // every plane: load them once (L2) and keep them in registers for the
   // CTA's planes, so the plane loop issues no global loads.
@@ -221,6 +251,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
     for (int m = 0; m < E; ++m) dst[m * st] = v[m];
   }
 }
+#endif
 
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
 template <int N, int C, int E_>
@@ -267,6 +298,9 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
 }
 
+#ifndef HOLO_FWD_RECUR
+#define HOLO_FWD_RECUR 1
+#endif
 // K5 with TMA staging (N <= 1024): one elected thread streams plane k+1's
 // C-column block (N rows x C complex) into the other half of a double-buffered
 // shared-memory stage with 2D tensor copies while the CTA transforms plane k,
@@ -319,6 +353,16 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
+#if HOLO_FWD_RECUR
+  // conj H_k carried from plane to plane: h *= conj G (see k_adj_cols)
+  float2 h[E], g[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const uint64_t t = tab[p0 + m * st];
+    h[m] = cis_cycles(plane_phase(t, k0 + kb), circ);
+    g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+  }
+#endif
   for (int k = kb; k < ke; ++k) {
     const int b = (k - kb) & 1;
     // the other stage was last read in the previous plane, before fft_line's barriers
@@ -339,6 +383,13 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = src[(j + m * TPF) * C];
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
+#if HOLO_FWD_RECUR
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      acc[m] = cadd(acc[m], cmulc(v[m], h[m]));
+      h[m] = cmul(h[m], g[m]);
+    }
+#else
 #pragma unroll
     for (int m0 = 0; m0 < E; m0 += 4) {
 #pragma unroll
@@ -346,6 +397,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
         acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ)));
       asm volatile("" ::: "memory");
     }
+#endif
   }
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
@@ -997,13 +1049,14 @@ cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, 
   return err ? err : cudaGetLastError();
 }
 
-#ifndef HOLO_ADJ_PPC
-#define HOLO_ADJ_PPC 64
-#endif
+// planes per CTA in the column passes = H_k recurrence length (error bound)
+constexpr int kMaxRecur = 32;
+#define HOLO_ADJ_PPC kMaxRecur
 // 4 columns (256 threads) per CTA: with R / phase held in registers across the
 // CTA's planes (126 registers) two CTAs fit per SM (measured best at 1024^2)
 #define HOLO_ADJ_C(N) 4
-#define HOLO_FWD_C(N) ((N) >= 1024 ? 8 : 4)
+// 4 columns (256 threads, ~240 registers: acc, conj H_k and its step in registers)
+#define HOLO_FWD_C(N) 4
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
@@ -1032,6 +1085,7 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
 int fwd_groups(const Plan& p, int nzl) {
   const int tiles = std::max(1, p.nx / HOLO_FWD_C(p.ny));
   int g = (16 * 148 + tiles - 1) / tiles;  // ~8 waves of 2 CTAs/SM: small tail
+  g = std::max(g, (nzl + kMaxRecur - 1) / kMaxRecur);  // H_k recurrence length <= kMaxRecur planes
   g = std::max(1, std::min(g, nzl));
   return std::min(g, 64);
 }
