@@ -500,6 +500,8 @@ struct Engine {
       a.tau_tv = (float)(step * cfg.lambda_tv);
       a.lr_tv = a.tau_tv > 0.f ? (float)(1.0 / (8.0 * (step * cfg.lambda_tv))) : 0.f;
       a.real_mode = cfg.real_nonnegative ? 1 : 0;
+      // ip / dx2 feed only the sufficient-decrease test, which is analytic below 1/(2 sigma^2)
+      a.ipdx = (cfg.step_policy == HOLO_POLICY_BACKTRACKING && 2.0 * sigma2 * step > 1.0 + 1e-14) ? 1 : 0;
       HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzl, 1), s));
       if ((rc = prox_step(a, s))) return rc;
       if ((rc = read_scalars(s))) return rc;

@@ -47,6 +47,7 @@ struct ProxArgs {
   // region + halo read back by the next pass)
   int tile_h = 0;                   // strip kernel: tile height (tile = width)
   float rcp_tx = 0.f, rcp_tpp = 0.f;  // strip kernel: 1/tiles_x, 1/tiles_per_plane (fast division)
+  int ipdx = 1;                      // 0: skip <g, dx> and |dx|^2 (no evaluated backtracking test)
   int t0 = 0, t1 = 0, pass_len = 0;  // pass_len 0: single pass
   float2* vbuf = nullptr;            // v = y - step grad (first pass writes)
   float4* sbuf = nullptr;            // (p, q) per pixel, two halves (pass parity)

@@ -498,17 +498,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t
       up1 = p[s][1];
       if (!(rInt & (1u << s))) continue;
       const long long g = g0 + (long long)s * a.nx;
-      const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
-      float2 y[2] = {lo2(y4), hi2(y4)};
-      if (a.beta != 0.f) {
-        const float4 o = staged ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
-        y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
-        y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
-      }
-      float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.grad) gr4 = staged ? slot(2, s) : *reinterpret_cast<const float4*>(a.grad + g);
-      if (a.real_mode) gr4.y = gr4.w = 0.f;
-      const float2 gr[2] = {lo2(gr4), hi2(gr4)};
       {
         const float2 nx2 = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
         acc[PT_TVX] += nx2.x + nx2.y;
@@ -516,8 +505,21 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t
         const float2 re = make_float2(p[s][0].x, p[s][1].x), im = make_float2(p[s][0].y, p[s][1].y);
         const float2 m2 = fma2(re, re, mul2(im, im));
         acc[PT_L1] += sqrt_a(m2.x) + sqrt_a(m2.y);
+      }
+      if (a.ipdx) {  // <g, x_new - y> and |x_new - y|^2: only for an evaluated backtracking test
+        const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
+        float2 y[2] = {lo2(y4), hi2(y4)};
+        if (a.beta != 0.f) {
+          const float4 o = staged ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
+          y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
+          y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
+        }
+        float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.grad) gr4 = staged ? slot(2, s) : *reinterpret_cast<const float4*>(a.grad + g);
+        if (a.real_mode) gr4.y = gr4.w = 0.f;
+        const float2 gr[2] = {lo2(gr4), hi2(gr4)};
         const float2 dx0 = sub2(p[s][0], y[0]), dx1 = sub2(p[s][1], y[1]);
-        const float2 ip = fma2(gr[0], dx0, mul2(gr[1], dx1));       // (re, im) parts of <g, dx>
+        const float2 ip = fma2(gr[0], dx0, mul2(gr[1], dx1));  // (re, im) parts of <g, dx>
         const float2 d2 = fma2(dx0, dx0, mul2(dx1, dx1));
         acc[PT_IP] += ip.x + ip.y;
         acc[PT_DX2] += d2.x + d2.y;
