@@ -305,16 +305,21 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t
         const float2 gy0 = sub2(v[s][0], up0), gy1 = sub2(v[s][1], up1);
         up0 = v[s][0];
         up1 = v[s][1];
+        // One rsqrt per part serves both the guard's |Dv| and the projection:
+        // r = 1/|Dv|, |Dv| = |Dv|^2 r, and lr Dv / max(1, lr |Dv|) = min(lr, r) Dv.
+        const float2 n0 = fma2(gy0, gy0, mul2(gx0, gx0)), n1 = fma2(gy1, gy1, mul2(gx1, gx1));
+        const float2 r0 = make_float2(rsqrt_a(fmaxf(n0.x, 1e-30f)), rsqrt_a(fmaxf(n0.y, 1e-30f)));
+        const float2 r1 = make_float2(rsqrt_a(fmaxf(n1.x, 1e-30f)), rsqrt_a(fmaxf(n1.y, 1e-30f)));
         // guard: G = tau TV(w) + |w - v|^2 / 2 - tau TV(v) per part, here the -tau TV(v) term
         if (rInt & (1u << s)) {
-          const float2 nv = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
+          const float2 nv = fma2(n0, r0, mul2(n1, r1));
           acc[PT_G_R] = fmaf(-ttv, nv.x, acc[PT_G_R]);
           acc[PT_G_I] = fmaf(-ttv, nv.y, acc[PT_G_I]);
         }
-        float2 pn0 = mul2(lr2, gy0), qn0 = mul2(lr2, gx0);
-        float2 pn1 = mul2(lr2, gy1), qn1 = mul2(lr2, gx1);
-        project(pn0, qn0);
-        project(pn1, qn1);
+        const float2 f0 = make_float2(fminf(lr2.x, r0.x), fminf(lr2.x, r0.y));
+        const float2 f1 = make_float2(fminf(lr2.x, r1.x), fminf(lr2.x, r1.y));
+        const float2 pn0 = mul2(f0, gy0), qn0 = mul2(f0, gx0);
+        const float2 pn1 = mul2(f1, gy1), qn1 = mul2(f1, gx1);
         p[s][0] = rp[s][0] = pn0;
         q[s][0] = rq[s][0] = qn0;
         p[s][1] = rp[s][1] = pn1;
