@@ -240,7 +240,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # HOLO_NCCL_SINGLE_RANK=1 runs the sharded (NCCL) path even with one rank
+    sharded = world > 1 or os.environ.get("HOLO_NCCL_SINGLE_RANK") == "1"
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_1904_04884_b200 import _native as nat
@@ -255,14 +257,14 @@ def main():
     geom = VolumeGeometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
     # identical synthetic hologram on every rank (seeded), generated on the GPU
     b = make_hologram(cfg, dev) if rank == 0 or world == 1 else None
-    if world > 1:
+    if sharded:
         bt = torch.as_tensor(b if b is not None else np.zeros((ny, nx)), dtype=torch.float64, device=dev)
         dist.broadcast(bt, 0)
         b = bt.cpu().numpy()
     scfg = SolverConfig(weights=RegularizerWeights(l1, tv), max_iters=iters, tv_inner_iters=inner)
     ncfg = native_config(scfg)
     lib = nat.load()
-    if world > 1:
+    if sharded:
         nid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             buf = ctypes.create_string_buffer(128)
@@ -283,7 +285,7 @@ def main():
         rep = one_solve()
     lib.holo_profile_enable(eng.h, 1)
     launches0 = lib.holo_launch_count()
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -295,11 +297,11 @@ def main():
             vox_iters += nx * ny * nz * rep.iterations
         ev1.record(stream)
         torch.cuda.synchronize(dev)
-    if world > 1:
+    if sharded:
         dist.barrier()
     launches = lib.holo_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -374,7 +376,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     eng.close()
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

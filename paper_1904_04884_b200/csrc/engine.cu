@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -753,7 +754,10 @@ int holo_nccl_unique_id(void* out128) {
 int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_unique_id, int rank, int nranks,
                         holo_handle** out) {
   if (!geom || !out) return fail(HOLO_ERR_INVALID, "null argument");
-  if (nranks == 1) return holo_create(geom, device, out);
+  // one rank needs no communicator; HOLO_NCCL_SINGLE_RANK=1 keeps the NCCL path
+  // anyway so the sharded plumbing can be exercised on a single GPU (tests)
+  const char* force = std::getenv("HOLO_NCCL_SINGLE_RANK");
+  if (nranks == 1 && !(force && force[0] == '1')) return holo_create(geom, device, out);
 #ifdef HOLO_WITH_NCCL
   if (!nccl_unique_id) return fail(HOLO_ERR_INVALID, "null nccl id");
   if (!holo::nccl().ok) return fail(HOLO_ERR_NCCL, "libnccl.so.2 not loadable");

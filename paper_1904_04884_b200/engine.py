@@ -7,6 +7,7 @@ straight through the C ABI.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -39,7 +40,8 @@ class HoloEngine:
         g = nat.geometry(geom)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            if shard is None or shard[1] == 1:
+            single = os.environ.get("HOLO_NCCL_SINGLE_RANK") == "1"  # exercise NCCL with one rank
+            if shard is None or (shard[1] == 1 and not single):
                 nat.check(self.lib.holo_create(ctypes.byref(g), self.device, ctypes.byref(h)), "holo_create")
             else:
                 rank, nranks, nid = shard
