@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #ifdef HOLO_WITH_NCCL
@@ -218,6 +219,9 @@ struct Engine {
   int32_t* coo_cols = nullptr;
   double2* coo_vals = nullptr;
   long long coo_cap = 0;
+  // pinned double buffer for device -> pageable-host exports (lazy)
+  void* stage_host[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   double real_sigma2 = -1.0;  // cached ||A_real||^2
   // results of the last solve
   int ix = 0;  // slot holding the solution
@@ -236,6 +240,12 @@ struct Engine {
     cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(fgp_beta);
     cudaFree(coo_counts); cudaFree(coo_offsets);
     cudaFree(coo_rows); cudaFree(coo_cols); cudaFree(coo_vals);
+    for (int i = 0; i < 2; ++i) {
+      if (stage_host[i]) cudaFreeHost(stage_host[i]);
+      if (stage_ev[i]) cudaEventDestroy(stage_ev[i]);
+      stage_host[i] = nullptr;
+      stage_ev[i] = nullptr;
+    }
     cudaFree(mp_v); cudaFree(mp_s); cudaFree(mp_r); cudaFree(mp_tvv);
     plan_free(plan);
 #ifdef HOLO_WITH_NCCL
@@ -851,6 +861,49 @@ int holo_plane_nnz(holo_handle* h, int64_t* nnz_per_local_plane) {
   })
 }
 
+// memcpy split over host threads (the destination is fresh pageable memory:
+// the copy also takes its first-touch page faults, which parallelise)
+static void par_memcpy(char* dst, const char* src, size_t n) {
+  static const int nt = (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+  if (nt <= 1 || n < (size_t)(4u << 20)) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t part = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * part;
+    if (o >= n) break;
+    pool.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(part, n - o)); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Device -> pageable host through a pinned double buffer: the DMA of chunk
+// i+1 overlaps the threaded copy-out of chunk i (pageable cudaMemcpy runs at a
+// few GB/s; this path is bounded by the host copy-out).
+static int d2h_staged(Engine& e, void* dst, const void* src, size_t n, cudaStream_t s) {
+  constexpr size_t kChunk = 32u << 20;
+  for (int i = 0; i < 2; ++i) {
+    if (!e.stage_host[i]) HOLO_CUDA(cudaHostAlloc(&e.stage_host[i], kChunk, cudaHostAllocDefault));
+    if (!e.stage_ev[i]) HOLO_CUDA(cudaEventCreateWithFlags(&e.stage_ev[i], cudaEventDisableTiming));
+  }
+  const size_t nchunk = (n + kChunk - 1) / kChunk;
+  auto issue = [&](size_t c) -> cudaError_t {
+    const size_t o = c * kChunk, len = std::min(kChunk, n - o);
+    cudaError_t err = cudaMemcpyAsync(e.stage_host[c & 1], (const char*)src + o, len, cudaMemcpyDeviceToHost, s);
+    return err ? err : cudaEventRecord(e.stage_ev[c & 1], s);
+  };
+  for (size_t c = 0; c < std::min<size_t>(2, nchunk); ++c) HOLO_CUDA(issue(c));
+  for (size_t c = 0; c < nchunk; ++c) {
+    HOLO_CUDA(cudaEventSynchronize(e.stage_ev[c & 1]));
+    const size_t o = c * kChunk, len = std::min(kChunk, n - o);
+    par_memcpy((char*)dst + o, (const char*)e.stage_host[c & 1], len);
+    if (c + 2 < nchunk) HOLO_CUDA(issue(c + 2));
+  }
+  return HOLO_OK;
+}
+
 static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, void* vals, int64_t cap, int64_t* nnz, bool host,
                       cudaStream_t s) {
   Engine& e = h->e;
@@ -880,11 +933,9 @@ static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, void* vals, 
   // values widened to complex128 on the device: the caller's arrays are final
   HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, e.coo_rows, e.coo_cols, nullptr,
                               e.coo_vals, s));
-  HOLO_CUDA(cudaMemcpyAsync(rows, e.coo_rows, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
-  HOLO_CUDA(cudaMemcpyAsync(cols, e.coo_cols, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost, s));
-  HOLO_CUDA(cudaMemcpyAsync(vals, e.coo_vals, sizeof(double2) * tot, cudaMemcpyDeviceToHost, s));
-  HOLO_CUDA(cudaStreamSynchronize(s));
-  return HOLO_OK;
+  if ((rc = d2h_staged(e, rows, e.coo_rows, sizeof(int32_t) * tot, s))) return rc;
+  if ((rc = d2h_staged(e, cols, e.coo_cols, sizeof(int32_t) * tot, s))) return rc;
+  return d2h_staged(e, vals, e.coo_vals, sizeof(double2) * tot, s);
 }
 
 int holo_export_coo_host(holo_handle* h, int32_t* rows, int32_t* cols, double* vals, int64_t cap, int64_t* nnz) {
