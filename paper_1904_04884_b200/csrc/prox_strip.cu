@@ -175,14 +175,36 @@ HD void band_wait(uint64_t* bars, int i, unsigned& bph) {
   bph ^= 1u << i;
 }
 
+// Later passes of a multi-pass FGP stage the dual state instead: v (8 B),
+// (p, q) and (rp, rq) (16 B each) per pixel, 160 KB per region, in one slot
+// (read into registers by the prologue, after which the next region's state
+// streams in while this region iterates).
+constexpr int kStateV = 0, kStateS = RH * RW / 2, kStateR = kStateS + RH * RW;  // float4 offsets
+constexpr unsigned kStateBytes = (unsigned)(RH * RW) * 40u;
+HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t* bar, const Work& wk) {
+  const int c1 = wk.plane * a.ny + wk.tg.ri0;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(kStateBytes)
+               : "memory");
+  const int off[3] = {kStateV, kStateS, kStateR}, c0[3] = {2 * wk.tg.rj0, 4 * wk.tg.rj0, 4 * wk.tg.rj0};
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(slot + off[k])),
+        "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0[k]), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // One region.  `pre` is its staged input slot (first / single pass) or null
 // (later passes of a multi-pass FGP read HBM directly).
 // EDGE: the region touches a plane edge, so its outer rows/columns need the
 // exact replicated-edge rule; otherwise they are garbage zone and the
 // lane-0 / lane-31 / band-0 / band-(NW-1) selects are skipped.
 template <bool TV, bool EDGE, int PH>
-__device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t* bbar, unsigned& bph, const float4* pre,
-                                          int work, const Work& wk) {
+__device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
+                                          unsigned& bph, float4* pre, uint64_t* sbar, int work, const Work& wk,
+                                          int next_work) {
   const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
   const TileGeom& tg = wk.tg;
@@ -216,22 +238,27 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, Bands& sm, uint64_t
   // neighbouring regions of the same launch still read as their halo
   const float4* s_in = a.sbuf + ((pass - 1) & 1) * a.sstride;
   const float4* r_in = a.rbuf + ((pass - 1) & 1) * a.sstride;
-  if (!first) {  // later pass of a multi-pass FGP: v and the dual state from HBM
+  if (!first) {  // later pass of a multi-pass FGP: v and the dual state from the staged slot
+    (void)s_in;
+    (void)r_in;
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
-      const long long g = g0 + (long long)s * a.nx;
-      const float4 vv = *reinterpret_cast<const float4*>(a.vbuf + g);
+      const int row = r0 + s;
+      const float4 vv = pre[kStateV + row * (RW / 2) + lane];
       v[s][0] = lo2(vv);
       v[s][1] = hi2(vv);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const float4 sq = s_in[g + k], rr = r_in[g + k];
+        const float4 sq = pre[kStateS + row * RW + 2 * lane + k], rr = pre[kStateR + row * RW + 2 * lane + k];
         p[s][k] = lo2(sq);
         q[s][k] = hi2(sq);
         rp[s][k] = lo2(rr);
         rq[s][k] = hi2(rr);
       }
     }
+    // the slot is free once everyone has read it: stream the next region's state in
+    __syncthreads();
+    if (threadIdx.x == 0 && next_work >= 0) tma_state(a, maps, pre, sbar, work_geom(a, next_work));
   } else {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
 #pragma unroll
@@ -601,14 +628,19 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   if (work < 0) return;
   const bool leader = threadIdx.x == 0;
   if (leader) {
-    mbar_init(&bars[0], 1);
+    mbar_init(&bars[0], 1);  // slot 0 (and the later passes' state slot)
     mbar_init(&bars[1], 1);
     mbar_init(&bbar[0], NW);
     mbar_init(&bbar[1], NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (staged && leader) tma_region(a, maps, pre, &bars[0], work_geom(a, work));
+  if (leader) {
+    if (staged)
+      tma_region(a, maps, pre, &bars[0], work_geom(a, work));
+    else
+      tma_state(a, maps, pre, &bars[0], work_geom(a, work));
+  }
   unsigned phase = 0;  // bit b: parity of slot b's next completion
   unsigned bph = 0;    // bit b: parity of band barrier b's next completion
   for (int buf = 0; work >= 0; buf ^= 1) {
@@ -617,21 +649,21 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     if (staged && leader && nw >= 0)
       tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], work_geom(a, nw));
     const Work cur = work_geom(a, work);
-    const float4* slot = staged ? pre + buf * kSlotArrays * kSlotF4 : nullptr;
-    if (staged) {
-      mbar_wait(&bars[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-    }
+    // x / x_prev / grad slots double-buffered (first pass); one state slot (later passes)
+    const int sb = staged ? buf : 0;
+    float4* slot = pre + sb * kSlotArrays * kSlotF4;
+    mbar_wait(&bars[sb], (phase >> sb) & 1u);
+    phase ^= 1u << sb;
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, sm, bbar, bph, slot, work, cur);
+      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw);
     else
-      prox_tile<TV, false, PH>(a, sm, bbar, bph, slot, work, cur);
+      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw);
     work = nw;
   }
 }
 
 // 2D view [nplanes * ny rows][2 nx floats] of one complex64 stack, 64 x 128 boxes
-CUresult encode_map(CUtensorMap* m, const void* base, int ny_total, int nx) {
+CUresult encode_map(CUtensorMap* m, const void* base, int ny_total, int nx, int fpp = 2) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -641,9 +673,10 @@ CUresult encode_map(CUtensorMap* m, const void* base, int ny_total, int nx) {
       return CUDA_ERROR_NOT_FOUND;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const cuuint64_t dims[2] = {(cuuint64_t)2 * nx, (cuuint64_t)ny_total};
-  const cuuint64_t strides[1] = {(cuuint64_t)2 * nx * sizeof(float)};
-  const cuuint32_t box[2] = {2 * RW, RH};
+  // fpp floats per pixel: 2 (complex64 x, v), 4 (float4 dual state)
+  const cuuint64_t dims[2] = {(cuuint64_t)fpp * nx, (cuuint64_t)ny_total};
+  const cuuint64_t strides[1] = {(cuuint64_t)fpp * nx * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)(fpp * RW), RH};
   const cuuint32_t estr[2] = {1, 1};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -699,11 +732,17 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(Bands) + sizeof(float4) * 2 * kSlotArrays * kSlotF4;
   TmaMaps maps;
   memset(&maps, 0, sizeof(maps));
-  if (a.pass_len == 0 || a.t0 == 0) {  // staged passes
-    const int rows = a.nplanes * a.ny;
+  const int rows = a.nplanes * a.ny;
+  if (a.pass_len == 0 || a.t0 == 0 || !(a.tau_tv > 0.f)) {  // x, x_prev, grad
     if (encode_map(&maps.m[0], a.x, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
     if (a.beta != 0.f && encode_map(&maps.m[1], a.xp, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
     if (a.grad && encode_map(&maps.m[2], a.grad, rows, a.nx) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  } else {  // later passes: v and the dual state half written by the previous pass
+    const long long half = ((a.t0 / a.pass_len - 1) & 1) * a.sstride;
+    if (encode_map(&maps.m[0], a.vbuf, rows, a.nx) != CUDA_SUCCESS ||
+        encode_map(&maps.m[1], a.sbuf + half, rows, a.nx, 4) != CUDA_SUCCESS ||
+        encode_map(&maps.m[2], a.rbuf + half, rows, a.nx, 4) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
   }
   const long long total = (long long)a.tiles_per_plane * a.nplanes;
   const int grid = (int)std::min<long long>(total, nsm);
