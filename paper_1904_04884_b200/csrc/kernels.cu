@@ -180,20 +180,19 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
   for (int m = 0; m < E; ++m) out[base + m * st] = cscale(v[m], scale);
 }
 
-#ifndef HOLO_ADJ_RECUR
-#define HOLO_ADJ_RECUR 1
-#endif
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
 template <int N, int C, int E_>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const float2* __restrict__ R,
-                                                                    float2* __restrict__ out, int nx, long long P,
-                                                                    int k0, int nzl, int ppc,
+                                                                    const __grid_constant__ CUtensorMap out_map,
+                                                                    int nx, int ny, int k0, int nzl, int ppc,
                                                                     const uint64_t* __restrict__ tab,
                                                                     const float4* __restrict__ twg,
                                                                     const float2* __restrict__ circg) {
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
-  extern __shared__ float2 smem[];
+  constexpr int BOX_ROWS = N < 256 ? N : 256;
+  static_assert(N * C <= (N + N / E_) * C, "output stage fits in the exchange buffer");
+  extern __shared__ __align__(128) float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* circ = smem + 2 * N;
   float2* buf = smem + 2 * N + 256;
@@ -203,11 +202,11 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
-#if HOLO_ADJ_RECUR
+  const bool leader = threadIdx.x == 0;
   // H_{k+1} = H_k * G with G = cis(2 pi dz q) per pixel: R H_k is carried from
   // plane to plane by one complex multiply (the reference's TransferLadder
   // recurrence, optics.py:146-169), exact cis() only at the CTA's first plane
-  // (<= HOLO_ADJ_PPC steps: < 4e-6 relative drift worst case).
+  // (<= kMaxRecur steps: < 4e-6 relative drift worst case).
   const int kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
   float2 r[E], g[E];
 #pragma unroll
@@ -223,35 +222,30 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
       v[m] = r[m];
       r[m] = cmul(r[m], g[m]);
     }
+    // the previous plane's TMA store must have read the stage (= buf) before
+    // fft_line's first barrier lets anyone write buf again
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     fft_line<N, true, E_>(v, j, buf + c, C, tw);
-    float2* dst = out + (long long)k * P + p0;
+    // dense [row][C] stage, then one bulk tensor store per 256 rows: the
+    // column block leaves as full boxes instead of C x 8-byte row segments
+    __syncthreads();  // the last FFT pass read buf
 #pragma unroll
-    for (int m = 0; m < E; ++m) dst[m * st] = v[m];
+    for (int m = 0; m < E; ++m) buf[(j + m * TPF) * C + c] = v[m];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (leader) {
+#pragma unroll
+      for (int r0 = 0; r0 < N; r0 += BOX_ROWS)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                         reinterpret_cast<uint64_t>(&out_map)),
+                     "r"(2 * (int)blockIdx.x * C), "r"(k * ny + r0),
+                     "r"((unsigned)__cvta_generic_to_shared(buf + r0 * C))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
   }
+  if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // smem outlives the reads
 }
-#else
-  // R and the packed phase of this thread's column elements are the same for
-  // every plane: load them once (L2) and keep them in registers for the
-  // CTA's planes, so the plane loop issues no global loads.
-  float2 r[E];
-  uint64_t ph[E];
-#pragma unroll
-  for (int m = 0; m < E; ++m) {
-    r[m] = R[p0 + m * st];
-    ph[m] = tab[p0 + m * st];
-  }
-  const int kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
-  for (int k = kb; k < ke; ++k) {
-    float2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = cmul(r[m], cis_cycles(plane_phase(ph[m], k0 + k), circ));
-    fft_line<N, true, E_>(v, j, buf + c, C, tw);
-    float2* dst = out + (long long)k * P + p0;
-#pragma unroll
-    for (int m = 0; m < E; ++m) dst[m * st] = v[m];
-  }
-}
-#endif
 
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
 template <int N, int C, int E_>
@@ -1071,8 +1065,13 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
       const long long blocks = p.nx / C;
       const int ppc = (int)std::max(1LL, std::min<long long>(HOLO_ADJ_PPC, blocks * nzl / (148LL * 8)));
       dim3 grid(p.nx / C, (nzl + ppc - 1) / ppc);
+      CUtensorMap map;
+      if (encode_tiled_2d(&map, out, 2 * p.nx, (long long)nzl * p.ny, 2 * C, N < 256 ? N : 256)) {
+        err = cudaErrorInvalidValue;
+        return;
+      }
       err = set_smem(k_adj_cols<N, C, E>, smem);
-      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, out, p.nx, p.P, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()],
+      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, map, p.nx, p.ny, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()],
                                                   p.circle);
     };
     launch(std::integral_constant<int, HOLO_ADJ_C(N)>());  // nx >= 8 always
