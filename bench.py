@@ -346,7 +346,7 @@ def main():
             nnz = vol.nnz
         e_s = time.perf_counter() - t0
         e2e = {"value": e_vox / e_s, "unit": "voxel-iter/s", "h2d_bytes_per_step": 8 * nx * ny,
-               "d2h_bytes_per_step": 16 * nnz + 8 * nz + 8 * iters, "steps": e2e_steps}
+               "d2h_bytes_per_step": 24 * nnz + 8 * nz + 8 * iters, "steps": e2e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
