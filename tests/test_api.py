@@ -54,3 +54,26 @@ def test_sparse_containers():
     assert vol.nnz == sp.nnz and vol.planes[1].nnz == 0
     assert np.array_equal(vol.to_dense()[0], p)
     assert isinstance(SparseVolume.zeros(g).planes[0], SparsePlane)
+
+
+def test_axpy_exact_merge():
+    """axpy = alpha x + y with the reference's entry-set semantics (sparsevol.py:146-176):
+    (row, col) order, coincident entries summed, exact cancellations dropped."""
+    from paper_1904_04884_b200.sparsevol import axpy
+    rng = np.random.default_rng(5)
+    g = VolumeGeometry(9, 6, 3, 1e-5, 1e-5, 5e-3, 632e-9)
+    a = (rng.standard_normal((3, 6, 9)) + 1j * rng.standard_normal((3, 6, 9))) * (rng.random((3, 6, 9)) < 0.3)
+    b = (rng.standard_normal((3, 6, 9)) + 1j * rng.standard_normal((3, 6, 9))) * (rng.random((3, 6, 9)) < 0.3)
+    b[0, 1, 2] = -(1.5 - 0.5j) * 2.0  # exact cancellation against alpha * a
+    a[0, 1, 2] = 2.0
+    alpha = 1.5 - 0.5j
+    x, y = SparseVolume.from_dense_stack(a, g), SparseVolume.from_dense_stack(b, g)
+    z = axpy(alpha, x, y)
+    want = alpha * a + b
+    assert np.array_equal(z.to_dense(), want)
+    for zp, wp in zip(z.planes, want):
+        zp.validate()
+        assert zp.nnz == int(np.count_nonzero(wp))  # the cancelled entry is gone
+    assert axpy(0, x, y).nnz == y.nnz
+    with pytest.raises(ValueError):
+        axpy(1.0, x, SparseVolume.zeros(VolumeGeometry(9, 6, 4, 1e-5, 1e-5, 5e-3, 632e-9)))
