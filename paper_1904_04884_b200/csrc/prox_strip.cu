@@ -501,21 +501,27 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 
   // soft threshold of w (fix-up pass: identity part where the guard fired); x_new -> p
   const float tl = a.tau_l1;
+  // |x_new| = gsc |w| = gsc n2 rsqrt(n2) feeds the L1 sum with the same rsqrt
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
+    float l1 = 0.f;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const float wr = (force & 1u) ? v[s][k].x : rp[s][k].x;
       const float wi = (force & 2u) ? v[s][k].y : rp[s][k].y;
       if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
         p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
+        l1 += p[s][k].x;
         continue;
       }
       const float n2 = fmaf(wr, wr, wi * wi);
-      const float shrink = 1.f - tl * rsqrt_a(n2);
+      const float r = rsqrt_a(fmaxf(n2, 1e-30f));
+      const float shrink = 1.f - tl * r;
       const float gsc = (tl > 0.f) ? ((n2 > tl * tl) ? shrink : 0.f) : 1.f;
       p[s][k] = make_float2(wr * gsc, wi * gsc);
+      l1 = fmaf(gsc * n2, r, l1);
     }
+    if (rInt & (1u << s)) acc[PT_L1] += l1;
   }
   sm.bot[0][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
   __syncthreads();
@@ -534,10 +540,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       {
         const float2 nx2 = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
         acc[PT_TVX] += nx2.x + nx2.y;
-        // |x| of both columns: (re^2 + im^2) packed as (col 0, col 1)
-        const float2 re = make_float2(p[s][0].x, p[s][1].x), im = make_float2(p[s][0].y, p[s][1].y);
-        const float2 m2 = fma2(re, re, mul2(im, im));
-        acc[PT_L1] += sqrt_a(m2.x) + sqrt_a(m2.y);
       }
       if (a.ipdx) {  // <g, x_new - y> and |x_new - y|^2: only for an evaluated backtracking test
         const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
