@@ -515,24 +515,33 @@ struct Engine {
       a.ipdx = (cfg.step_policy == HOLO_POLICY_BACKTRACKING && 2.0 * sigma2 * step > 1.0 + 1e-14) ? 1 : 0;
       HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzl, 1), s));
       if ((rc = prox_step(a, s))) return rc;
-      if ((rc = read_scalars(s))) return rc;
-      // guard fix-up: planes whose TV output was worse than its input take the
-      // identity for that part (prox.py:138-147); rare, so handled out of line
-      while (h_scal[SC_FAIL] > 0.5) {
-        last.guard_fixups += 1;
-        ProxArgs f = a;
-        f.force = force_acc;
-        if ((rc = prox_step(f, s))) return rc;
-        if ((rc = read_scalars(s))) return rc;
+      // forward of the candidate (the adjoint scratch is consumed, reuse it)
+      // and its data term, queued behind the prox without a host round trip:
+      // the guard flag is read back together with f_new
+      auto forward_fnew = [&]() -> int {
+        int r2 = forward_spectrum(X[c], S[c], s);
+        if (r2) return r2;
+        HOLO_CUDA(prof.begin(PK_SENSOR, s));
+        HOLO_CUDA(sensor(plan, S[c], nullptr, 1.f, 0.f, Bspec, nullptr, sens_part, s));
+        HOLO_CUDA(final_sum(sens_part, sens_nblk, 1.0 / (double)P, scal + SC_FNEW, s));
+        HOLO_CUDA(prof.end(s));
+        return read_scalars(s);
+      };
+      if ((rc = forward_fnew())) return rc;
+      if (h_scal[SC_FAIL] > 0.5) {
+        // guard fix-up: planes whose TV output was worse than its input take the
+        // identity for that part (prox.py:138-147); rare, so the speculative
+        // forward above is simply redone
+        do {
+          last.guard_fixups += 1;
+          ProxArgs f = a;
+          f.force = force_acc;
+          if ((rc = prox_step(f, s))) return rc;
+          if ((rc = read_scalars(s))) return rc;
+        } while (h_scal[SC_FAIL] > 0.5);
+        if ((rc = forward_fnew())) return rc;
       }
       last.attempts += 1;
-      // forward of the candidate; the adjoint scratch is consumed, reuse it
-      if ((rc = forward_spectrum(X[c], S[c], s))) return rc;
-      HOLO_CUDA(prof.begin(PK_SENSOR, s));
-      HOLO_CUDA(sensor(plan, S[c], nullptr, 1.f, 0.f, Bspec, nullptr, sens_part, s));
-      HOLO_CUDA(final_sum(sens_part, sens_nblk, 1.0 / (double)P, scal + SC_FNEW, s));
-      HOLO_CUDA(prof.end(s));
-      if ((rc = read_scalars(s))) return rc;
       out.slot = c;
       out.f_new = h_scal[SC_FNEW];
       out.f_y = h_scal[SC_FY];
