@@ -81,6 +81,14 @@ int holo_create(const holo_geometry* geom, int device, holo_handle** out);
 int holo_nccl_unique_id(void* out128);
 int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_unique_id, int rank, int nranks,
                         holo_handle** out);
+/* In-process rank group on one GPU (tests and diagnostics; no reference
+ * counterpart): nranks (<= 8) handles out[0..nranks) own planes
+ * [r*nz/nranks, (r+1)*nz/nranks) exactly like holo_create_sharded, but their
+ * spectrum / scalar allreduce is an event-ordered device sum instead of NCCL.
+ * Each handle must be driven from its own host thread (holo_solve* blocks in
+ * the collective until every member arrives), each on its own stream.  Destroy
+ * every handle with holo_destroy. */
+int holo_create_local_group(const holo_geometry* geom, int device, int nranks, holo_handle** out);
 int holo_destroy(holo_handle* h);
 int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end);
 

@@ -60,6 +60,8 @@ SIGNATURES = {
     "holo_nccl_unique_id": (ctypes.c_int, [_P]),
     "holo_create_sharded": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, _P, ctypes.c_int, ctypes.c_int,
                                            ctypes.POINTER(_H)]),
+    "holo_create_local_group": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int,
+                                               ctypes.POINTER(_H)]),
     "holo_destroy": (ctypes.c_int, [_H]),
     "holo_local_planes": (ctypes.c_int, [_H, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "holo_operator_norm": (ctypes.c_int, [_H, _I, ctypes.POINTER(_D)]),

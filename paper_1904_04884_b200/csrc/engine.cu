@@ -19,6 +19,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -169,6 +172,81 @@ struct Prof {
     HOLO_CUDA(prof.end((s)));                \
   } while (0)
 
+// In-process rank group (holo_create_local_group): N engines on one GPU, each
+// driven by its own host thread and stream, whose two collectives (spectrum and
+// scalar allreduce) are an event-ordered device sum instead of NCCL.  Every
+// member records an event after producing its buffer and blocks on the host
+// until all members have; the last one makes its stream wait for all events,
+// sums the buffers in rank order into each member's buffer, and records `done`,
+// which every member's stream then waits on.  No kernel waits on another
+// kernel: only stream/event ordering, so the sharded code path (plane ranges,
+// partial spectra, scalar reductions, shared control decisions, per-rank COO)
+// runs on one GPU exactly as it does under NCCL.
+constexpr int kMaxGroup = 8;
+struct GroupPtrs {
+  const void* src[kMaxGroup];
+  void* dst[kMaxGroup];
+};
+template <class T>
+__global__ void k_group_sum(const GroupPtrs gp, int n, long long count) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    T acc = static_cast<const T*>(gp.src[0])[i];
+    for (int r = 1; r < n; ++r) acc += static_cast<const T*>(gp.src[r])[i];
+    for (int r = 0; r < n; ++r) static_cast<T*>(gp.dst[r])[i] = acc;
+  }
+}
+
+struct LocalGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  void* buf[kMaxGroup] = {};
+  cudaEvent_t ev[kMaxGroup] = {};
+  cudaEvent_t done = nullptr;
+  int refs = 0;
+  ~LocalGroup() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (done) cudaEventDestroy(done);
+  }
+  cudaError_t init(int nn) {
+    n = nn;
+    cudaError_t e;
+    for (int r = 0; r < n; ++r)
+      if ((e = cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming))) return e;
+    return cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  }
+  // sum over members of buf (count elements of T), in place on every member
+  template <class T>
+  cudaError_t allreduce(int r, T* b, long long count, cudaStream_t s) {
+    std::unique_lock<std::mutex> lk(m);
+    buf[r] = b;
+    cudaError_t e = cudaEventRecord(ev[r], s);
+    if (e) return e;
+    const long long my_gen = gen;
+    if (++arrived == n) {
+      for (int i = 0; i < n; ++i)
+        if ((e = cudaStreamWaitEvent(s, ev[i], 0))) return e;
+      GroupPtrs gp{};
+      for (int i = 0; i < n; ++i) gp.src[i] = gp.dst[i] = buf[i];
+      const int threads = 256;
+      const int blocks = (int)std::min<long long>((count + threads - 1) / threads, 148LL * 8);
+      k_group_sum<T><<<std::max(blocks, 1), threads, 0, s>>>(gp, n, count);
+      if ((e = cudaGetLastError())) return e;
+      if ((e = cudaEventRecord(done, s))) return e;
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my_gen; });
+      if ((e = cudaStreamWaitEvent(s, done, 0))) return e;
+    }
+    return cudaSuccess;
+  }
+};
+
 // host scalar block (pinned) layout
 enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_AUX, SC_N };
 
@@ -181,6 +259,7 @@ struct Engine {
 #ifdef HOLO_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  std::shared_ptr<LocalGroup> lgroup;  // in-process rank group (tests), else NCCL
   // volume buffers
   float2* X[3] = {nullptr, nullptr, nullptr};
   float2* scratch = nullptr;
@@ -368,6 +447,10 @@ struct Engine {
   // ---- collectives (no-ops on one rank) ----
   int allreduce_spec(float2* spec, cudaStream_t s) {
     if (nranks == 1) return HOLO_OK;
+    if (lgroup) {
+      HOLO_CUDA(lgroup->allreduce<float>(rank, reinterpret_cast<float*>(spec), P * 2, s));
+      return HOLO_OK;
+    }
 #ifdef HOLO_WITH_NCCL
     HOLO_NCCL(ncclAllReduce(spec, spec, (size_t)P * 2, ncclFloat, ncclSum, comm, s));
     return HOLO_OK;
@@ -377,6 +460,10 @@ struct Engine {
   }
   int allreduce_scalars(double* d, int n, cudaStream_t s) {
     if (nranks == 1) return HOLO_OK;
+    if (lgroup) {
+      HOLO_CUDA(lgroup->allreduce<double>(rank, d, n, s));
+      return HOLO_OK;
+    }
 #ifdef HOLO_WITH_NCCL
     HOLO_NCCL(ncclAllReduce(d, d, n, ncclDouble, ncclSum, comm, s));
     return HOLO_OK;
@@ -802,6 +889,36 @@ int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_
   (void)device; (void)nccl_unique_id; (void)rank;
   return fail(HOLO_ERR_UNSUPPORTED, "built without NCCL");
 #endif
+}
+
+int holo_create_local_group(const holo_geometry* geom, int device, int nranks, holo_handle** out) {
+  if (!geom || !out) return fail(HOLO_ERR_INVALID, "null argument");
+  if (nranks < 1 || nranks > holo::kMaxGroup) return fail(HOLO_ERR_INVALID, "nranks must be in [1, 8]");
+  TRY({
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce) return fail(HOLO_ERR_CUDA, cudaGetErrorString(ce));
+    auto grp = std::make_shared<holo::LocalGroup>();
+    ce = grp->init(nranks);
+    if (ce) return fail(HOLO_ERR_CUDA, cudaGetErrorString(ce));
+    for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+    for (int r = 0; r < nranks; ++r) {
+      auto* h = new holo_handle();
+      int rc = h->e.init(*geom, device, r, nranks);
+      if (rc) {
+        std::string keep = g_err;
+        delete h;
+        for (int q = 0; q < r; ++q) {
+          delete out[q];
+          out[q] = nullptr;
+        }
+        g_err = keep;
+        return rc;
+      }
+      h->e.lgroup = grp;
+      out[r] = h;
+    }
+    return HOLO_OK;
+  })
 }
 
 int holo_destroy(holo_handle* h) {

@@ -53,6 +53,29 @@ class HoloEngine:
         nat.check(self.lib.holo_local_planes(h, ctypes.byref(kb), ctypes.byref(ke)))
         self.k_begin, self.k_end = kb.value, ke.value
 
+    @classmethod
+    def local_group(cls, geom, nranks: int, device: int | None = None) -> list["HoloEngine"]:
+        """``nranks`` z-shards of one geometry on ONE GPU whose two collectives
+        are in-process device sums (holo_create_local_group): the sharded code
+        path of ``shard=`` without NCCL, for tests.  Drive each engine's solve
+        from its own thread (the solves meet in every collective)."""
+        lib = nat.load()
+        torch = _torch()
+        dev = torch.cuda.current_device() if device is None else int(device)
+        g = nat.geometry(geom)
+        hs = (ctypes.c_void_p * nranks)()
+        with torch.cuda.device(dev):
+            nat.check(lib.holo_create_local_group(ctypes.byref(g), dev, nranks, hs), "holo_create_local_group")
+        out = []
+        for r in range(nranks):
+            e = cls.__new__(cls)
+            e.lib, e.geom, e.device, e.h = lib, geom, dev, ctypes.c_void_p(hs[r])
+            kb, ke = ctypes.c_int32(), ctypes.c_int32()
+            nat.check(lib.holo_local_planes(e.h, ctypes.byref(kb), ctypes.byref(ke)))
+            e.k_begin, e.k_end = kb.value, ke.value
+            out.append(e)
+        return out
+
     @property
     def nz_local(self) -> int:
         return self.k_end - self.k_begin
