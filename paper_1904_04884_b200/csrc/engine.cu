@@ -392,7 +392,7 @@ struct Engine {
     a.nplanes = nplanes;
     if (!prox_supported(ny, nx, inner))
       return fail(HOLO_ERR_UNSUPPORTED, "tv_inner_iters=" + std::to_string(inner) + " too deep for the single-pass prox tile");
-    const size_t need = (size_t)std::max(nplanes, 1) * a.tiles_per_plane * kProxParts;
+    const size_t need = (size_t)std::max(nplanes, 1) * a.tiles_per_plane * kProxParts * std::max(1, (a.part_warps + 1) / 2);
     if (need > prox_part_cap) {
       cudaFree(prox_part);
       prox_part = nullptr;

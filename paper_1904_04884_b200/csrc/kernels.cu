@@ -676,7 +676,9 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
 
 constexpr int kReduceThreads = 128;
 
-__global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __restrict__ part, int tpp,
+// part: per tile fp64 sums (generic kernel, nw == 0) or per (tile, warp) fp32
+// sums (strip kernel, nw warps per tile), summed here in fp64
+__global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __restrict__ part, int tpp, int nw,
                                                                 double tau, int tv_on, uint8_t* __restrict__ force_acc,
                                                                 double* __restrict__ plane_out,
                                                                 int* __restrict__ new_fail) {
@@ -684,10 +686,23 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
   double acc[kProxParts];
 #pragma unroll
   for (int i = 0; i < kProxParts; ++i) acc[i] = 0.0;
-  const double* src = part + (long long)plane * tpp * kProxParts;
-  for (int t = threadIdx.x; t < tpp; t += kReduceThreads) {
+  if (nw > 0) {  // [part][tile][warp]: coalesced float4 rows per part
+    const long long n = (long long)tpp * nw;
+    const float* src = reinterpret_cast<const float*>(part) + (long long)plane * kProxParts * n;
 #pragma unroll
-    for (int i = 0; i < kProxParts; ++i) acc[i] += src[(long long)t * kProxParts + i];
+    for (int i = 0; i < kProxParts; ++i) {
+      const float4* s4 = reinterpret_cast<const float4*>(src + i * n);
+      for (long long t = threadIdx.x; t < n / 4; t += kReduceThreads) {
+        const float4 f = s4[t];
+        acc[i] += ((double)f.x + (double)f.y) + ((double)f.z + (double)f.w);
+      }
+    }
+  } else {
+    const double* src = part + (long long)plane * tpp * kProxParts;
+    for (int t = threadIdx.x; t < tpp; t += kReduceThreads) {
+#pragma unroll
+      for (int i = 0; i < kProxParts; ++i) acc[i] += src[(long long)t * kProxParts + i];
+    }
   }
   __shared__ double s[kProxParts];
   block_sum<kProxParts, kReduceThreads>(acc, s);
@@ -1204,8 +1219,8 @@ cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
 
 cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
                         int* new_fail, cudaStream_t s) {
-  k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, tau_tv, tv_on, force_acc, plane_out,
-                                                     new_fail);
+  k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, a.kind == 1 ? a.part_warps : 0,
+                                                     tau_tv, tv_on, force_acc, plane_out, new_fail);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

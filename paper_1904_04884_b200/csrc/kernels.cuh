@@ -41,7 +41,9 @@ struct ProxArgs {
   const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule (device)
   float fgpb[16] = {};              // same schedule by value (strip kernel, inner <= 12)
   const uint8_t* force = nullptr;   // guard fix-up pass: per plane bit0 re / bit1 im -> identity
-  double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts]
+  double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts] doubles, or (part_warps > 0)
+                                    // [nplanes][kProxParts][tiles_per_plane][part_warps] floats
+  int part_warps = 0;
   // multi-pass FGP (strip kernel, large T): this launch runs iterations [t0, t1);
   // the dual state crosses launches through HBM (interior pixels written,
   // region + halo read back by the next pass)

@@ -116,6 +116,39 @@ HD Work work_geom(const ProxArgs& a, int work) {
   return wk;
 }
 
+// The leader computes the next region's geometry anyway (for its TMA copies)
+// and publishes it in shared memory; the other 511 threads read it instead of
+// repeating the divisions.
+struct GeoSlot {
+  int plane, i0, i1, j0, j1, ri0, rj0, pad;
+};
+HD void geo_store(GeoSlot& g, const Work& wk) {
+  g.plane = wk.plane;
+  g.i0 = wk.tg.i0;
+  g.i1 = wk.tg.i1;
+  g.j0 = wk.tg.j0;
+  g.j1 = wk.tg.j1;
+  g.ri0 = wk.tg.ri0;
+  g.rj0 = wk.tg.rj0;
+}
+HD Work geo_load(const ProxArgs& a, const GeoSlot& g) {
+  const int4 lo = *reinterpret_cast<const int4*>(&g.plane);
+  const int4 hi = *reinterpret_cast<const int4*>(&g.j1);
+  Work wk;
+  wk.plane = lo.x;
+  TileGeom& t = wk.tg;
+  t.i0 = lo.y;
+  t.i1 = lo.z;
+  t.j0 = lo.w;
+  t.j1 = hi.x;
+  t.ri0 = hi.y;
+  t.rj0 = hi.z;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  wk.g0 = (long long)wk.plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
+  wk.edge = t.rj0 == 0 || t.rj0 + RW == a.nx || t.ri0 == 0 || t.ri0 + RH == a.ny;
+  return wk;
+}
+
 // Region inputs are staged by TMA: one elected thread loads the 64x64
 // complex box of x, x_prev and grad (32 KB each, row-major [row][2*col]
 // floats) into a double-buffered slot with one 2D tensor copy per array,
@@ -205,7 +238,7 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
 template <bool TV, bool EDGE, int PH>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
                                           unsigned& bph, float4* pre, uint64_t* sbar, int work, const Work& wk,
-                                          int next_work) {
+                                          int next_work, const GeoSlot* nxgeo) {
   const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
   const TileGeom& tg = wk.tg;
@@ -259,7 +292,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     }
     // the slot is free once everyone has read it: stream the next region's state in
     __syncthreads();
-    if (threadIdx.x == 0 && next_work >= 0) tma_state(a, maps, pre, sbar, work_geom(a, next_work));
+    if (threadIdx.x == 0 && next_work >= 0) tma_state(a, maps, pre, sbar, geo_load(a, *nxgeo));
   } else {
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta), cs = splat2(-a.step);
 #pragma unroll
@@ -575,7 +608,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     acc[PT_G_R] += a.tvv[(long long)work * 2];
     acc[PT_G_I] += a.tvv[(long long)work * 2 + 1];
   }
-  __shared__ float wsum[NW][kProxParts];
   {
     float r8[8];
 #pragma unroll
@@ -594,20 +626,16 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     x += __shfl_xor_sync(0xffffffffu, x, 2);
     x += __shfl_xor_sync(0xffffffffu, x, 1);
     const int slot = (lane >> 2) & 7;
-    if ((lane & 3) == 0 && slot < kProxParts) wsum[w][slot] = x;
+    // per-warp fp32 partials straight to HBM; k_prox_reduce sums them in fp64
+    // (no cross-warp barrier at the end of the region)
+    if ((lane & 3) == 0 && slot < kProxParts)
+      reinterpret_cast<float*>(a.part)[(((long long)plane * kProxParts + slot) * a.tiles_per_plane + tile) * NW + w] = x;
   }
-  __syncthreads();
-  // fp64 across the warps: 16 lanes per part (parts 2w', 2w'+1 in warp w')
-  static_assert(NW <= 16 && kProxParts % 2 == 0, "");
-  if (threadIdx.x < 16 * kProxParts) {
-    const int part = threadIdx.x >> 4, k = threadIdx.x & 15;
-    double t = k < NW ? (double)wsum[k][part] : 0.0;
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (k == 0) a.part[((long long)plane * a.tiles_per_plane + tile) * kProxParts + part] = t;
-  }
-  // No trailing barrier: every band / slot read of this region precedes the
-  // barrier above, and wsum is rewritten only after the next region's barriers.
+  // The next region's leader refills this region's x / grad slot right away:
+  // when the epilogue read the slot (evaluated backtracking test), wait for
+  // every warp first.  Band slots and geo[] are only rewritten behind the next
+  // region's own barriers.
+  if (a.ipdx) __syncthreads();
 }
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
@@ -620,6 +648,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   float4* pre = dyn + sizeof(Bands) / sizeof(float4);
   __shared__ uint64_t bars[2];   // TMA slot completion
   __shared__ uint64_t bbar[2];   // band-slot split barrier (one arrival per warp)
+  __shared__ __align__(16) GeoSlot geo[2];  // [buf] geometry of the region in slot buf
   constexpr bool staged = PH <= 1;
   const int total = a.tiles_per_plane * a.nplanes;
   auto next_from = [&](int t) {
@@ -636,31 +665,36 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     mbar_init(&bbar[0], NW);
     mbar_init(&bbar[1], NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    geo_store(geo[0], work_geom(a, work));
   }
   __syncthreads();
   if (leader) {
+    const Work w0 = geo_load(a, geo[0]);
     if (staged)
-      tma_region(a, maps, pre, &bars[0], work_geom(a, work));
+      tma_region(a, maps, pre, &bars[0], w0);
     else
-      tma_state(a, maps, pre, &bars[0], work_geom(a, work));
+      tma_state(a, maps, pre, &bars[0], w0);
   }
   unsigned phase = 0;  // bit b: parity of slot b's next completion
   unsigned bph = 0;    // bit b: parity of band barrier b's next completion
   for (int buf = 0; work >= 0; buf ^= 1) {
     const int nw = next_from(work + gridDim.x);
-    // the other slot was last read by the previous region, before its final barrier
-    if (staged && leader && nw >= 0)
-      tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], work_geom(a, nw));
-    const Work cur = work_geom(a, work);
+    // geo[buf ^ 1] and the other slot were last read by the previous region, before its final barrier
+    if (leader && nw >= 0) {
+      const Work wn = work_geom(a, nw);
+      geo_store(geo[buf ^ 1], wn);
+      if (staged) tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], wn);
+    }
+    const Work cur = geo_load(a, geo[buf]);
     // x / x_prev / grad slots double-buffered (first pass); one state slot (later passes)
     const int sb = staged ? buf : 0;
     float4* slot = pre + sb * kSlotArrays * kSlotF4;
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw);
+      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1]);
     else
-      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw);
+      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1]);
     work = nw;
   }
 }
@@ -730,6 +764,7 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.tiles_per_plane = a.tiles_x * ((ny + a.tile_h - 1) / a.tile_h);
   a.rcp_tx = 1.f / (float)a.tiles_x;
   a.rcp_tpp = 1.f / (float)a.tiles_per_plane;
+  a.part_warps = NW;
 }
 
 cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
