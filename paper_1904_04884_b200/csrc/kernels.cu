@@ -271,37 +271,46 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
-  for (int k = kb; k < ke; ++k) {
+  // Horner from the last plane, as in k_fwd_cols_staged
+  float zx[E];
+  float2 zyy[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const uint64_t t = tab[p0 + m * st];
+    const float2 g = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+    zx[m] = g.x;
+    zyy[m] = make_float2(g.y, -g.y);
+  }
+  for (int k = ke - 1; k >= kb; --k) {
     float2 v[E];
     const float2* src = in + (long long)k * P + p0;
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = src[m * st];
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
-    // transfer multiply-accumulate in chunks of 4: bounds the table loads in
-    // flight (16 B each) so acc[] + v[] stay in registers
 #pragma unroll
-    for (int m0 = 0; m0 < E; m0 += 4) {
-#pragma unroll
-      for (int m = m0; m < m0 + 4 && m < E; ++m)
-        acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ)));
-      asm volatile("" ::: "memory");
-    }
+    for (int m = 0; m < E; ++m) acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
   }
+#pragma unroll
+  for (int m = 0; m < E; ++m)
+    acc[m] = cmulc(acc[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + kb), circ));
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
 }
 
-#ifndef HOLO_FWD_RECUR
-#define HOLO_FWD_RECUR 1
-#endif
 // K5 with TMA staging (N <= 1024): one elected thread streams plane k+1's
 // C-column block (N rows x C complex) into the other half of a double-buffered
 // shared-memory stage with 2D tensor copies while the CTA transforms plane k,
 // so the column loads leave the critical path (the plain kernel waited on HBM
 // once per plane with only 16 warps per SM to hide it).
 template <int N, int C, int E_>
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged(
+// 2 columns per CTA (128 threads) at <= 160 registers: 3 CTAs / 12 warps per
+// SM (4 columns at 190 registers fit one CTA / 8 warps: 14.5 vs 12.3 ms per 10
+// C3 iterations)
+#ifndef HOLO_FWD_MINB
+#define HOLO_FWD_MINB 3
+#endif
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_FWD_MINB) k_fwd_cols_staged(
     const __grid_constant__ CUtensorMap in_map, float2* __restrict__ Spart, int nx, long long P, int ny, int nzl,
     int ppg, int k0, const uint64_t* __restrict__ tab, const float4* __restrict__ twg,
     const float2* __restrict__ circg) {
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (leader && kb < ke) issue(kb, 0);
+  if (leader && kb < ke) issue(ke - 1, 0);  // planes are walked last to first (Horner)
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
@@ -347,22 +356,26 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
-#if HOLO_FWD_RECUR
-  // conj H_k carried from plane to plane: h *= conj G (see k_adj_cols)
-  float2 h[E], g[E];
+  // sum_k v_k conj(H_k) over the CTA's planes = conj(H_kb) sum_k v_k z^(k-kb),
+  // z = conj(G) = cis(-2 pi dz q) (the reference's ladder step, optics.py:146-169):
+  // Horner from the last plane, acc <- acc z + v_k, one complex FMA pair per
+  // element and plane; z is held as z.x and the pair (-z.y, z.y) so that
+  // acc z = swap(acc) (-z.y, z.y) + acc z.x needs no sign shuffles.
+  float zx[E];
+  float2 zyy[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const uint64_t t = tab[p0 + m * st];
-    h[m] = cis_cycles(plane_phase(t, k0 + kb), circ);
-    g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+    const float2 g = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+    zx[m] = g.x;
+    zyy[m] = make_float2(g.y, -g.y);
   }
-#endif
-  for (int k = kb; k < ke; ++k) {
-    const int b = (k - kb) & 1;
+  for (int k = ke - 1; k >= kb; --k) {
+    const int i = ke - 1 - k, b = i & 1;
     // the other stage was last read in the previous plane, before fft_line's barriers
-    if (leader && k + 1 < ke) issue(k + 1, b ^ 1);
+    if (leader && k - 1 >= kb) issue(k - 1, b ^ 1);
     {
-      const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]), par = ((k - kb) >> 1) & 1;
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]), par = (i >> 1) & 1;
       unsigned done = 0;
       do {
         asm volatile(
@@ -377,22 +390,13 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, 1) k_fwd_cols_staged
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = src[(j + m * TPF) * C];
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
-#if HOLO_FWD_RECUR
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-      acc[m] = cadd(acc[m], cmulc(v[m], h[m]));
-      h[m] = cmul(h[m], g[m]);
-    }
-#else
-#pragma unroll
-    for (int m0 = 0; m0 < E; m0 += 4) {
-#pragma unroll
-      for (int m = m0; m < m0 + 4 && m < E; ++m)
-        acc[m] = cadd(acc[m], cmulc(v[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + k), circ)));
-      asm volatile("" ::: "memory");
-    }
-#endif
+    for (int m = 0; m < E; ++m) acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
   }
+  // times conj(H_kb), exact (64-bit phase)
+#pragma unroll
+  for (int m = 0; m < E; ++m)
+    acc[m] = cmulc(acc[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + kb), circ));
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
@@ -1064,8 +1068,12 @@ constexpr int kMaxRecur = 32;
 // 4 columns (256 threads) per CTA: with R / phase held in registers across the
 // CTA's planes (126 registers) two CTAs fit per SM (measured best at 1024^2)
 #define HOLO_ADJ_C(N) 4
-// 4 columns (256 threads, ~240 registers: acc, conj H_k and its step in registers)
-#define HOLO_FWD_C(N) 4
+// staged (N <= 1024): 2 columns per CTA, 3 CTAs per SM (see k_fwd_cols_staged);
+// direct loads (N > 1024): 4 columns, 32-byte row segments per warp load
+#ifndef HOLO_FWD_CC
+#define HOLO_FWD_CC 2
+#endif
+#define HOLO_FWD_C(N) ((N) <= 1024 ? HOLO_FWD_CC : 4)
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
