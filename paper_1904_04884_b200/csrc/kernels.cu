@@ -215,6 +215,11 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const flo
     r[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(t, k0 + kb), circ));
     g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
   }
+#ifndef HOLO_ADJ_UNROLL
+#define HOLO_ADJ_UNROLL 2  // alternating register roles for r / v: 12.69 -> 12.48 ms per 10 C3 iterations
+#endif
+  constexpr int kUnroll = HOLO_ADJ_UNROLL;
+#pragma unroll kUnroll
   for (int k = kb; k < ke; ++k) {
     float2 v[E];
 #pragma unroll
