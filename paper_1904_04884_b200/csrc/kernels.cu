@@ -181,8 +181,11 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
 }
 
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
+#ifndef HOLO_ADJ_MINB
+#define HOLO_ADJ_MINB 2  // 2 CTAs / 16 warps per SM at <= 128 registers (12.48 -> 12.32 ms per 10 C3 iterations)
+#endif
 template <int N, int C, int E_>
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_adj_cols(const float2* __restrict__ R,
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_ADJ_MINB) k_adj_cols(const float2* __restrict__ R,
                                                                     const __grid_constant__ CUtensorMap out_map,
                                                                     int nx, int ny, int k0, int nzl, int ppc,
                                                                     const uint64_t* __restrict__ tab,
@@ -1072,7 +1075,10 @@ constexpr int kMaxRecur = 32;
 #define HOLO_ADJ_PPC kMaxRecur
 // 4 columns (256 threads) per CTA: with R / phase held in registers across the
 // CTA's planes (126 registers) two CTAs fit per SM (measured best at 1024^2)
-#define HOLO_ADJ_C(N) 4
+#ifndef HOLO_ADJ_CC
+#define HOLO_ADJ_CC 4
+#endif
+#define HOLO_ADJ_C(N) HOLO_ADJ_CC
 // staged (N <= 1024): 2 columns per CTA, 3 CTAs per SM (see k_fwd_cols_staged);
 // direct loads (N > 1024): 4 columns, 32-byte row segments per warp load
 #ifndef HOLO_FWD_CC
