@@ -1,8 +1,12 @@
 """Summarise an .ncu-rep (details page + SASS instruction mix) as text for profiles/."""
 import csv
+import os
 import io
 import subprocess
 import sys
+
+# NCU_K=<regex>: one kernel of a multi-kernel report
+_K = ["-k", "regex:" + os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
 from collections import Counter
 
 SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Compute Workload Analysis",
@@ -10,7 +14,7 @@ SECTIONS = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Comput
 
 
 def run(args):
-    return subprocess.run(["ncu", "-i"] + args, capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", args[0]] + _K + args[1:], capture_output=True, text=True).stdout
 
 
 def main(rep):

@@ -11,9 +11,12 @@ import os
 import subprocess
 import sys
 
+# NCU_K=<regex>: one kernel of a multi-kernel report
+_K = ["-k", "regex:" + os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+
 rep, cls, vox = sys.argv[1], sys.argv[2], int(sys.argv[3])
 out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(__file__), "..", "profiles", "r01_traffic.json")
-rows = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+rows = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep] + _K + ["--page", "raw", "--csv"], capture_output=True,
                                                   text=True).stdout)))
 d = dict(zip(rows[0], rows[2]))
 unit = dict(zip(rows[0], rows[1]))
