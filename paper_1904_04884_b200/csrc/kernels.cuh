@@ -44,6 +44,9 @@ struct ProxArgs {
   double* part = nullptr;           // [nplanes][tiles_per_plane][kProxParts] doubles, or (part_warps > 0)
                                     // [nplanes][kProxParts][tiles_per_plane][part_warps] floats
   int part_warps = 0;
+  int walk = 0;                      // strip kernel: column-strip walk (multi-pass FGP), see prox_strip.cu
+  int ky = 1;                        // strip kernel: regions per column strip (tiles_per_plane = tiles_x * ky)
+  float rcp_ky = 1.f;
   // multi-pass FGP (strip kernel, large T): this launch runs iterations [t0, t1);
   // the dual state crosses launches through HBM (interior pixels written,
   // region + halo read back by the next pass)

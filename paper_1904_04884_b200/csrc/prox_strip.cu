@@ -94,11 +94,40 @@ HD int fdiv(int n, int d, float rcp) {
 struct Work {
   int plane = -1;
   TileGeom tg;
-  long long g0;  // this thread's first element (row 0 of its band, column pair)
-  bool edge;     // region touches a plane edge
+  long long g0;    // this thread's first element (row 0 of its band, column pair)
+  bool edge;       // region touches a plane edge
+  int k = 0;       // strip walk: region index in its column strip (0: plane top)
+  int rsave = -1;  // strip walk: frame row the next region reads from above (-1: none)
 };
 
+// Strip walk (multi-pass FGP, a.walk): a CTA walks a column strip of a plane
+// top to bottom.  Region k's frame starts at row f0_k = min(k TH, ny - RH),
+// its tile is rows [k TH, (k+1) TH) (the last region: down to ny), and band 0
+// reads the rows above the frame from what region k-1 saved for every
+// exchange of the pass (v, X per FGP step, w, x_new), so only the bottom of a
+// frame is halo (TH = 56 instead of 48 for 7-step passes).  TH is a multiple
+// of SR, so the saved row is always the last row of one band.
+// Work index = strip * ky + k, strip = plane * tiles_x + tx (tile = tx * ky + k).
+HD Work work_geom_walk(const ProxArgs& a, int work) {
+  Work wk;
+  const int strip = fdiv(work, a.ky, a.rcp_ky);
+  wk.k = work - strip * a.ky;
+  wk.plane = fdiv(strip, a.tiles_x, a.rcp_tx);
+  const int tx = strip - wk.plane * a.tiles_x;
+  TileGeom& t = wk.tg;
+  t.i0 = wk.k * a.tile_h;
+  t.j0 = tx * a.tile;
+  t.i1 = wk.k + 1 == a.ky ? a.ny : t.i0 + a.tile_h;
+  t.j1 = min(a.nx, t.j0 + a.tile);
+  t.ri0 = min(t.i0, a.ny - RH);
+  t.rj0 = min(max(t.j0 - a.halo, 0), a.nx - RW);
+  wk.rsave = wk.k + 1 < a.ky ? min(t.i0 + a.tile_h, a.ny - RH) - 1 - t.ri0 : -1;
+  return wk;
+}
+
+template <bool WALK>
 HD Work work_geom(const ProxArgs& a, int work) {
+  if constexpr (WALK) return work_geom_walk(a, work);
   Work wk;
   wk.plane = fdiv(work, a.tiles_per_plane, a.rcp_tpp);
   const int tile = work - wk.plane * a.tiles_per_plane;
@@ -120,7 +149,7 @@ HD Work work_geom(const ProxArgs& a, int work) {
 // and publishes it in shared memory; the other 511 threads read it instead of
 // repeating the divisions.
 struct GeoSlot {
-  int plane, i0, i1, j0, j1, ri0, rj0, pad;
+  int plane, i0, i1, j0, j1, ri0, rj0, k, rsave, pad[3];
 };
 HD void geo_store(GeoSlot& g, const Work& wk) {
   g.plane = wk.plane;
@@ -130,7 +159,10 @@ HD void geo_store(GeoSlot& g, const Work& wk) {
   g.j1 = wk.tg.j1;
   g.ri0 = wk.tg.ri0;
   g.rj0 = wk.tg.rj0;
+  g.k = wk.k;
+  g.rsave = wk.rsave;
 }
+template <bool WALK = true>
 HD Work geo_load(const ProxArgs& a, const GeoSlot& g) {
   const int4 lo = *reinterpret_cast<const int4*>(&g.plane);
   const int4 hi = *reinterpret_cast<const int4*>(&g.j1);
@@ -146,6 +178,10 @@ HD Work geo_load(const ProxArgs& a, const GeoSlot& g) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   wk.g0 = (long long)wk.plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
   wk.edge = t.rj0 == 0 || t.rj0 + RW == a.nx || t.ri0 == 0 || t.ri0 + RH == a.ny;
+  if constexpr (WALK) {
+    wk.k = g.k;
+    wk.rsave = g.rsave;
+  }
   return wk;
 }
 
@@ -157,6 +193,13 @@ HD Work geo_load(const ProxArgs& a, const GeoSlot& g) {
 constexpr int kSlotF4 = RH * RW / 2;  // float4 per array per slot
 constexpr int kSlotArrays = 3;        // x, x_prev, grad
 constexpr unsigned kArrayBytes = kSlotF4 * 16;
+// Strip-walk kernels: x and grad double-buffered ([buf][x, grad]), x_prev in
+// one slot after them (refilled for the next region once this region's
+// prologue has read it), then the saved rows [region parity][slot][lane]:
+// slot 0 v, 1 + j the X read by FGP step tstart + j, kSaveW w, kSaveX x_new.
+constexpr int kXpSlot = 4 * kSlotF4;
+constexpr int kStageWalkF4 = 5 * kSlotF4;
+constexpr int kSaveW = 9, kSaveX = 10, kSaveSlots = 11;
 
 struct TmaMaps {
   CUtensorMap m[kSlotArrays];
@@ -194,6 +237,29 @@ HD void tma_region(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_
         "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
   }
+}
+
+// strip walk: x and grad into buffer `buf`; the barrier expects x_prev's bytes
+// too (tma_xprev, issued later, completes it)
+HD void tma_box(const TmaMaps& maps, int k, float4* dst, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+HD void tma_region_walk(const ProxArgs& a, const TmaMaps& maps, float4* buf, uint64_t* bar, const Work& wk) {
+  const int c0 = 2 * wk.tg.rj0, c1 = wk.plane * a.ny + wk.tg.ri0;
+  const unsigned bytes = kArrayBytes * (1u + (a.beta != 0.f) + (a.grad != nullptr));
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  tma_box(maps, 0, buf, bar, c0, c1);
+  if (a.grad) tma_box(maps, 2, buf + kSlotF4, bar, c0, c1);
+}
+HD void tma_xprev(const ProxArgs& a, const TmaMaps& maps, float4* stage, uint64_t* bar, const Work& wk) {
+  if (a.beta == 0.f) return;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  tma_box(maps, 1, stage + kXpSlot, bar, 2 * wk.tg.rj0, wk.plane * a.ny + wk.tg.ri0);
 }
 
 // Band-slot split barrier: mbarriers with one arrival per warp (lane 0, after
@@ -238,7 +304,9 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
 template <bool TV, bool EDGE, int PH>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
                                           unsigned& bph, float4* pre, uint64_t* sbar, int work, const Work& wk,
-                                          int next_work, const GeoSlot* nxgeo) {
+                                          int next_work, const GeoSlot* nxgeo, float4* stage, float4* save,
+                                          uint64_t* nbar) {
+  constexpr bool WALK = PH != 0;  // multi-pass kernels walk column strips
   const int plane = wk.plane, tile = work - plane * a.tiles_per_plane;
   const uint32_t force = a.force ? a.force[plane] : 0u;
   const TileGeom& tg = wk.tg;
@@ -260,10 +328,34 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   const bool cInt = gj >= j0 && gj < j1;
   const long long g0 = wk.g0;
   // this thread's float4 (2 columns) of row s of array k in the staged slot
-  auto slot = [&](int k, int s) { return pre[k * kSlotF4 + (r0 + s) * (RW / 2) + lane]; };
+  auto slot = [&](int k, int s) {
+    if constexpr (WALK) return (k == 1 ? stage + kXpSlot : pre + (k ? kSlotF4 : 0))[(r0 + s) * (RW / 2) + lane];
+    return pre[k * kSlotF4 + (r0 + s) * (RW / 2) + lane];
+  };
   constexpr bool staged = PH <= 1;
+  // Strip walk: band 0 reads the rows above the frame, saved by the previous
+  // region (rd), through bot[.][0], which it alone reads: it copies each saved
+  // row in just before it is needed.  Band `saver` saves its last row into wr
+  // for the next region at every exchange.
+  const bool top = wk.k == 0;
+  const bool band0 = w == 0, saver = WALK && w == wk.rsave / SR && wk.rsave >= 0;
+  const float4* rd = save + (wk.k & 1) * kSaveSlots * 32 + lane;
+  float4* wr = save + ((wk.k + 1) & 1) * kSaveSlots * 32 + lane;
+  auto save_rows = [&](int sl, const float2 (&arr)[SR][2]) {
+    if constexpr (WALK)
+      if (saver) wr[sl * 32] = f4(arr[SR - 1][0], arr[SR - 1][1]);
+  };
+  auto fetch_above = [&](int buf, int sl) {
+    if constexpr (WALK)
+      if (band0) sm.bot[buf][0][lane] = rd[sl * 32];
+  };
+  // plane top row (zero y-difference): every band-0 row of an EDGE region in
+  // the tiled kernel (a halo row unless the region is at the top), only the top
+  // region's in a strip walk
+  auto top_rule = [&]() { return EDGE && w == 0 && (!WALK || top); };
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
+  if (TV && PH == 1) fetch_above(1, 0);  // v above the frame, read by iteration 0
   // PH: pass kind of a multi-pass FGP (compile-time, so no kernel carries the
   // state handling it does not use): 0 single pass, 1 first, 2 middle, 3 last
   constexpr bool first = PH == 0 || PH == 1, last = PH == 0 || PH == 3;
@@ -335,7 +427,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     return r;
   };
   auto above_of = [&](int buf, int k, float2 self) -> float2 {
-    if (EDGE && w == 0) return self;  // region top row: zero y-difference
+    if (top_rule()) return self;
     const float4 b4 = sm.bot[buf][w][lane];
     return k ? hi2(b4) : lo2(b4);
   };
@@ -353,10 +445,19 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       x1 = fma2(mtau, sub2(add2(rp[SR - 1][1], rq[SR - 1][1]), rqr1), v[SR - 1][1]);
     };
     float2 xl0, xl1;
+    auto save_x = [&](int sl) {  // X of the band's last row, just published
+      if constexpr (WALK)
+        if (saver) wr[sl * 32] = f4(xl0, xl1);
+    };
+    const int tstart = first ? 1 : a.t0;
     if (first) {
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
     sm.bot[1][w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
+    save_rows(0, v);
     __syncthreads();
+    if constexpr (WALK) {  // every thread has read this region's x_prev: stream the next region's in
+      if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
+    }
     {
       float2 up0 = above_of(1, 0, v[0][0]), up1 = above_of(1, 1, v[0][1]);
 #pragma unroll
@@ -394,7 +495,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       xlast(xl0, xl1);
       sm.top[lastbuf][w][lane] = f4(rp[0][0], rp[0][1]);
       sm.bot[lastbuf][w + 1][lane] = f4(xl0, xl1);
+      save_x(1);
       band_arrive(&bbar[lastbuf]);
+      fetch_above(lastbuf, 1);  // read by band 0 itself only: after its arrival
     }
     // ---- iterations max(t0,1)..t1-1: one fused sweep down the band per iteration ----
     // Split barrier: rows 1..SR-2 only need this band's registers, so they are
@@ -402,7 +505,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     // neighbours' band data; rows 0 and SR-1 follow the wait.
     const float2 ptau = splat2(a.tau_tv);
 #pragma unroll 2
-    for (int t = first ? 1 : a.t0; t < a.t1; ++t) {
+    for (int t = tstart; t < a.t1; ++t) {
       const int b = (t - 1) & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
       // one row's dual update from its u, given the u of the row above
@@ -441,7 +544,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       {
         // u of the row above the band: X of the band above + tau * my row-0 rp
         float2 up0 = fma2(ptau, r00, lo2(x4)), up1 = fma2(ptau, r01, hi2(x4));
-        if (EDGE && w == 0) {  // region top row: zero y-difference
+        if (top_rule()) {  // plane top row: zero y-difference
           up0 = u[0][0];
           up1 = u[0][1];
         }
@@ -451,7 +554,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       xlast(xl0, xl1);
       sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
       sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
+      save_x(2 + t - tstart);
       band_arrive(&bbar[b ^ 1]);
+      fetch_above(b ^ 1, 2 + t - tstart);
       lastbuf = b ^ 1;
     }
     band_wait(bbar, lastbuf, bph);  // every band's last publication (and its reads of the other buffer) is done
@@ -503,6 +608,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       }
     }
     sm.bot[0][w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
+    save_rows(kSaveW, rp);
+    fetch_above(0, kSaveW);
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
@@ -557,7 +664,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     if (rInt & (1u << s)) acc[PT_L1] += l1;
   }
   sm.bot[0][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+  save_rows(kSaveX, p);
+  fetch_above(0, kSaveX);
   __syncthreads();
+  if constexpr (WALK && !TV) {  // (TV: issued after iteration 0's barrier)
+    if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
+  }
   {
     float2 up0 = above_of(0, 0, p[0][0]), up1 = above_of(0, 1, p[0][1]);
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta);
@@ -578,7 +690,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         const float4 y4 = staged ? slot(0, s) : *reinterpret_cast<const float4*>(a.x + g);
         float2 y[2] = {lo2(y4), hi2(y4)};
         if (a.beta != 0.f) {
-          const float4 o = staged ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
+          // (strip walk: x_prev's slot may already hold the next region's)
+          const float4 o = (staged && !WALK) ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
           y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
           y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
         }
@@ -643,20 +756,37 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 template <bool TV, int PH>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(NT <= 1024, "");
-  extern __shared__ __align__(1024) float4 dyn[];  // Bands, then [2][3][RH][RW/2] float4 staged slots
+  // Bands, then the staged slots: [2][x, x_prev, grad] (single pass), or the
+  // strip walk's [2][x, grad] + x_prev + saved rows (first pass) / state slot
+  // + saved rows (later passes)
+  extern __shared__ __align__(1024) float4 dyn[];
   Bands& sm = *reinterpret_cast<Bands*>(dyn);
   float4* pre = dyn + sizeof(Bands) / sizeof(float4);
+  float4* save = pre + kStageWalkF4;  // strip walk only
   __shared__ uint64_t bars[2];   // TMA slot completion
   __shared__ uint64_t bbar[2];   // band-slot split barrier (one arrival per warp)
   __shared__ __align__(16) GeoSlot geo[2];  // [buf] geometry of the region in slot buf
   constexpr bool staged = PH <= 1;
+  constexpr bool WALK = PH != 0;
   const int total = a.tiles_per_plane * a.nplanes;
   auto next_from = [&](int t) {
     if (a.force)
       while (t < total && !a.force[t / a.tiles_per_plane]) t += gridDim.x;
     return t < total ? t : -1;
   };
-  int work = next_from(blockIdx.x);
+  // strip walk: strips blockIdx.x, +gridDim.x, ..., each region by region
+  const int nstrips = a.tiles_x * a.nplanes;
+  auto strip_from = [&](int st) {
+    if (a.force)
+      while (st < nstrips && !a.force[fdiv(st, a.tiles_x, a.rcp_tx)]) st += gridDim.x;
+    return st < nstrips ? st * a.ky : -1;
+  };
+  auto next_of = [&](int wkid) {
+    if constexpr (!WALK) return next_from(wkid + gridDim.x);
+    const int st = fdiv(wkid, a.ky, a.rcp_ky);
+    return wkid + 1 < (st + 1) * a.ky ? wkid + 1 : strip_from(st + gridDim.x);
+  };
+  int work = WALK ? strip_from(blockIdx.x) : next_from(blockIdx.x);
   if (work < 0) return;
   const bool leader = threadIdx.x == 0;
   if (leader) {
@@ -665,36 +795,45 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     mbar_init(&bbar[0], NW);
     mbar_init(&bbar[1], NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    geo_store(geo[0], work_geom(a, work));
+    geo_store(geo[0], work_geom<WALK>(a, work));
   }
   __syncthreads();
   if (leader) {
     const Work w0 = geo_load(a, geo[0]);
-    if (staged)
+    if (WALK && staged) {
+      tma_region_walk(a, maps, pre, &bars[0], w0);
+      tma_xprev(a, maps, pre, &bars[0], w0);
+    } else if (staged) {
       tma_region(a, maps, pre, &bars[0], w0);
-    else
+    } else {
       tma_state(a, maps, pre, &bars[0], w0);
+    }
   }
   unsigned phase = 0;  // bit b: parity of slot b's next completion
   unsigned bph = 0;    // bit b: parity of band barrier b's next completion
   for (int buf = 0; work >= 0; buf ^= 1) {
-    const int nw = next_from(work + gridDim.x);
+    const int nw = next_of(work);
     // geo[buf ^ 1] and the other slot were last read by the previous region, before its final barrier
     if (leader && nw >= 0) {
-      const Work wn = work_geom(a, nw);
+      const Work wn = work_geom<WALK>(a, nw);
       geo_store(geo[buf ^ 1], wn);
-      if (staged) tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], wn);
+      if (WALK && staged)
+        tma_region_walk(a, maps, pre + (buf ^ 1) * 2 * kSlotF4, &bars[buf ^ 1], wn);
+      else if (staged)
+        tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], wn);
     }
-    const Work cur = geo_load(a, geo[buf]);
+    const Work cur = geo_load<WALK>(a, geo[buf]);
     // x / x_prev / grad slots double-buffered (first pass); one state slot (later passes)
     const int sb = staged ? buf : 0;
-    float4* slot = pre + sb * kSlotArrays * kSlotF4;
+    float4* slot = pre + sb * (WALK ? 2 : kSlotArrays) * kSlotF4;
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1]);
+      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+                              &bars[sb ^ 1]);
     else
-      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1]);
+      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+                               &bars[sb ^ 1]);
     work = nw;
   }
 }
@@ -756,12 +895,22 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   const int h_hi = tp ? h_lo : inner + (inner & 1);           // >= T, tile even
   a.halo = h_lo;
   a.tile = RW - h_lo - h_hi;
-  a.tile_h = RH - h_lo - h_hi;
   a.pass_len = tp;
   a.t0 = 0;
   a.t1 = inner;
   a.tiles_x = (nx + a.tile - 1) / a.tile;
-  a.tiles_per_plane = a.tiles_x * ((ny + a.tile_h - 1) / a.tile_h);
+  // multi-pass: strip walk, only the frame bottom is halo (Tp A-steps + the
+  // final D^T); single pass: square tiles with halo on every side
+  a.walk = tp > 0 && !getenv("HOLO_PROX_NOWALK");
+  if (a.walk) {
+    a.tile_h = (RH - (tp + 1)) / SR * SR;  // multiple of SR: the saved row ends a band
+    a.ky = ny > RH ? 1 + (ny - RH + a.tile_h - 1) / a.tile_h : 1;
+  } else {
+    a.tile_h = RH - h_lo - h_hi;
+    a.ky = (ny + a.tile_h - 1) / a.tile_h;
+  }
+  a.rcp_ky = 1.f / (float)a.ky;
+  a.tiles_per_plane = a.tiles_x * a.ky;
   a.rcp_tx = 1.f / (float)a.tiles_x;
   a.rcp_tpp = 1.f / (float)a.tiles_per_plane;
   a.part_warps = NW;
@@ -774,7 +923,9 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(Bands) + sizeof(float4) * 2 * kSlotArrays * kSlotF4;
+  static_assert(kStateBytes == sizeof(float4) * kStageWalkF4, "later passes' state slot = the walk stage area");
+  const size_t smem = a.walk ? sizeof(Bands) + sizeof(float4) * (kStageWalkF4 + 2 * kSaveSlots * 32)
+                             : sizeof(Bands) + sizeof(float4) * 2 * kSlotArrays * kSlotF4;
   TmaMaps maps;
   memset(&maps, 0, sizeof(maps));
   const int rows = a.nplanes * a.ny;
@@ -789,7 +940,8 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
         encode_map(&maps.m[2], a.rbuf + half, rows, a.nx, 4) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  const long long total = (long long)a.tiles_per_plane * a.nplanes;
+  const long long total = a.walk ? (long long)a.tiles_x * a.nplanes  // strips
+                                 : (long long)a.tiles_per_plane * a.nplanes;
   const int grid = (int)std::min<long long>(total, nsm);
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
@@ -797,6 +949,7 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return;
     kern<<<grid, NT, smem, s>>>(a, maps);
   };
+  if (a.tau_tv > 0.f && a.pass_len && !a.walk) return cudaErrorInvalidValue;  // multi-pass kinds walk strips
   if (a.tau_tv > 0.f && a.pass_len) {
     if (a.t0 == 0)
       launch(k_prox_strip<true, 1>);
@@ -807,7 +960,10 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
   } else if (a.tau_tv > 0.f) {
     launch(k_prox_strip<true, 0>);
   } else {
-    launch(k_prox_strip<false, 0>);  // no TV: no FGP passes
+    if (a.walk)  // no TV: no FGP passes, but the strip-walk tiling of this setup
+      launch(k_prox_strip<false, 1>);
+    else
+      launch(k_prox_strip<false, 0>);
   }
   if (e) return e;
   return cudaGetLastError();
