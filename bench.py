@@ -35,6 +35,7 @@ CONFIGS = {
     "c1": (256, 256, 64, 50, None, 0, 0.5, 0.2, 5, 20e-6),
     "c2": (1024, 1024, 256, 100, 0.05, 1, 0.5, 0.2, 5, 20e-6),
     "c3": (1024, 1024, 512, 100, 0.2, 2, 0.5, 0.2, 5, 20e-6),
+    "c4": (2048, 2048, 1000, 100, 0.05, 3, 0.5, 0.2, 5, 20e-6),  # 134 GB of state on one B200 (8 GPUs in BASELINE)
     "c5": (1024, 1024, 512, 100, 0.05, 4, 0.05, 1.0, 20, 20e-6),  # rods (microfibers), length 10 d
 }
 METRIC = "voxel-iterations/sec (1024²×512 fused-lasso FISTA) at 1/2/4/8 B200; % HBM roofline"
@@ -381,7 +382,7 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{a.config}: {nx}x{ny}x{nz} fused-lasso FISTA, {iters} iterations, "
                                    f"{n_particles(cfg)} particles d=20um, lambda=({l1},{tv}), T={inner}",
-                       "l2": "inputs larger than L2 (state 3 x 4.3 GB complex64)", "parallelism": f"z-shard x{world}"},
+                       "l2": f"inputs larger than L2 (state 3 x {nx * ny * nz * 8 / 1e9:.1f} GB complex64)", "parallelism": f"z-shard x{world}"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_voxel": KERNEL_BYTES[dom]},

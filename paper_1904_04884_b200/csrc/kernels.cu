@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
 #define HOLO_ADJ_MINB 2  // 2 CTAs / 16 warps per SM at <= 128 registers (12.48 -> 12.32 ms per 10 C3 iterations)
 #endif
 template <int N, int C, int E_>
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_ADJ_MINB) k_adj_cols(const float2* __restrict__ R,
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>::TPF <= 256 ? HOLO_ADJ_MINB : 1) k_adj_cols(const float2* __restrict__ R,
                                                                     const __grid_constant__ CUtensorMap out_map,
                                                                     int nx, int ny, int k0, int nzl, int ppc,
                                                                     const uint64_t* __restrict__ tab,
@@ -194,11 +194,13 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_ADJ_MINB) k_adj
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int BOX_ROWS = N < 256 ? N : 256;
-  static_assert(N * C <= (N + N / E_) * C, "output stage fits in the exchange buffer");
   extern __shared__ __align__(128) float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* circ = smem + 2 * N;
   float2* buf = smem + 2 * N + 256;
+  // output stage [N][C], separate from the FFT exchange buffer: plane k+1's
+  // transform runs while the bulk stores still read plane k's stage
+  float2* stage = buf + (((N + N / E_) * C + 15) & ~15);  // 128-byte aligned for the bulk stores
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
@@ -230,15 +232,14 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_ADJ_MINB) k_adj
       v[m] = r[m];
       r[m] = cmul(r[m], g[m]);
     }
-    // the previous plane's TMA store must have read the stage (= buf) before
-    // fft_line's first barrier lets anyone write buf again
-    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     fft_line<N, true, E_>(v, j, buf + c, C, tw);
     // dense [row][C] stage, then one bulk tensor store per 256 rows: the
-    // column block leaves as full boxes instead of C x 8-byte row segments
-    __syncthreads();  // the last FFT pass read buf
+    // column block leaves as full boxes instead of C x 8-byte row segments.
+    // The previous plane's stores must have read the stage first.
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncthreads();
 #pragma unroll
-    for (int m = 0; m < E; ++m) buf[(j + m * TPF) * C + c] = v[m];
+    for (int m = 0; m < E; ++m) stage[(j + m * TPF) * C + c] = v[m];
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (leader) {
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_ADJ_MINB) k_adj
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
                          reinterpret_cast<uint64_t>(&out_map)),
                      "r"(2 * (int)blockIdx.x * C), "r"(k * ny + r0),
-                     "r"((unsigned)__cvta_generic_to_shared(buf + r0 * C))
+                     "r"((unsigned)__cvta_generic_to_shared(stage + r0 * C))
                      : "memory");
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
@@ -1094,7 +1095,7 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
     auto launch = [&](auto cc) {
       constexpr int C = decltype(cc)::value;  // C x 8-byte row segments per warp load / store
       constexpr int NT = C * FftShape<N, E>::TPF;
-      const size_t smem = col_smem<N, C, E>(256);
+      const size_t smem = col_smem<N, C, E>(256) + sizeof(float2) * ((size_t)N * C + 16);  // + output stage
       // planes per CTA: >= ~8 waves of CTAs in the grid
       const long long blocks = p.nx / C;
       const int ppc = (int)std::max(1LL, std::min<long long>(HOLO_ADJ_PPC, blocks * nzl / (148LL * 8)));
