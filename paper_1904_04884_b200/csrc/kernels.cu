@@ -180,6 +180,10 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fft_cols(const flo
   for (int m = 0; m < E; ++m) out[base + m * st] = cscale(v[m], scale);
 }
 
+template <int N, int C, int E>
+constexpr bool adj_separate_stage() {
+  return sizeof(float2) * (2 * N + 256 + (size_t)(N + N / E) * C + (size_t)N * C + 16) <= 227 * 1024;
+}
 // K2: out[k] = column-IFFT( H_{k0+k} * R ), one plane per blockIdx.y
 #ifndef HOLO_ADJ_MINB
 #define HOLO_ADJ_MINB 2  // 2 CTAs / 16 warps per SM at <= 128 registers (12.48 -> 12.32 ms per 10 C3 iterations)
@@ -198,9 +202,11 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* circ = smem + 2 * N;
   float2* buf = smem + 2 * N + 256;
-  // output stage [N][C], separate from the FFT exchange buffer: plane k+1's
-  // transform runs while the bulk stores still read plane k's stage
-  float2* stage = buf + (((N + N / E_) * C + 15) & ~15);  // 128-byte aligned for the bulk stores
+  // output stage [N][C], separate from the FFT exchange buffer where it fits
+  // (N <= 2048): plane k+1's transform runs while the bulk stores still read
+  // plane k's stage; else the exchange buffer doubles as the stage
+  constexpr bool kSep = adj_separate_stage<N, C, E_>();
+  float2* stage = kSep ? buf + (((N + N / E_) * C + 15) & ~15) : buf;  // 128-byte aligned for the bulk stores
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
@@ -232,12 +238,15 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
       v[m] = r[m];
       r[m] = cmul(r[m], g[m]);
     }
+    // (shared stage: the previous plane's stores must have read buf before
+    // fft_line's first barrier lets anyone write it)
+    if (!kSep && leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     fft_line<N, true, E_>(v, j, buf + c, C, tw);
     // dense [row][C] stage, then one bulk tensor store per 256 rows: the
     // column block leaves as full boxes instead of C x 8-byte row segments.
     // The previous plane's stores must have read the stage first.
-    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    __syncthreads();
+    if (kSep && leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncthreads();  // (shared stage: the last FFT pass read buf)
 #pragma unroll
     for (int m = 0; m < E; ++m) stage[(j + m * TPF) * C + c] = v[m];
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -319,7 +328,7 @@ template <int N, int C, int E_>
 #ifndef HOLO_FWD_MINB
 #define HOLO_FWD_MINB 3
 #endif
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, HOLO_FWD_MINB) k_fwd_cols_staged(
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>::TPF <= 128 ? HOLO_FWD_MINB : 1) k_fwd_cols_staged(
     const __grid_constant__ CUtensorMap in_map, float2* __restrict__ Spart, int nx, long long P, int ny, int nzl,
     int ppg, int k0, const uint64_t* __restrict__ tab, const float4* __restrict__ twg,
     const float2* __restrict__ circg) {
@@ -1085,7 +1094,10 @@ constexpr int kMaxRecur = 32;
 #ifndef HOLO_FWD_CC
 #define HOLO_FWD_CC 2
 #endif
-#define HOLO_FWD_C(N) ((N) <= 1024 ? HOLO_FWD_CC : 4)
+#ifndef HOLO_FWD_STAGED_MAX
+#define HOLO_FWD_STAGED_MAX 2048
+#endif
+#define HOLO_FWD_C(N) ((N) <= HOLO_FWD_STAGED_MAX ? HOLO_FWD_CC : 4)
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
@@ -1095,7 +1107,8 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
     auto launch = [&](auto cc) {
       constexpr int C = decltype(cc)::value;  // C x 8-byte row segments per warp load / store
       constexpr int NT = C * FftShape<N, E>::TPF;
-      const size_t smem = col_smem<N, C, E>(256) + sizeof(float2) * ((size_t)N * C + 16);  // + output stage
+      const size_t smem =
+          col_smem<N, C, E>(256) + (adj_separate_stage<N, C, E>() ? sizeof(float2) * ((size_t)N * C + 16) : 0);
       // planes per CTA: >= ~8 waves of CTAs in the grid
       const long long blocks = p.nx / C;
       const int ppc = (int)std::max(1LL, std::min<long long>(HOLO_ADJ_PPC, blocks * nzl / (148LL * 8)));
@@ -1133,7 +1146,7 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
     constexpr int C = HOLO_FWD_C(N);  // acc[] + v[] stay in registers at <= 128 per thread
     constexpr int NT = C * FftShape<N, E>::TPF;
     dim3 grid(p.nx / C, groups);
-    if constexpr (N <= 1024) {
+    if constexpr (N <= HOLO_FWD_STAGED_MAX) {
       CUtensorMap map;
       if (encode_tiled_2d(&map, in, 2 * p.nx, (long long)nzl * p.ny, 2 * C, N < 256 ? N : 256)) {
         err = cudaErrorInvalidValue;
