@@ -354,6 +354,7 @@ def main():
                "h2d_bytes_per_step": 8 * nx * ny * world, "d2h_bytes_per_step": int(d2h_t.item()),
                "steps": e2e_steps, "path": "per-rank holo_solve (host b) + holo_export_coo_host"}
     if not a.no_e2e and world == 1 and not sharded:
+        eng.close()  # the public path builds its own engine (C4: 134 GB each)
         pinned = torch.empty((ny, nx), dtype=torch.float64, pin_memory=True)
         pinned.copy_(torch.as_tensor(b))
         field = ComplexField2D.__new__(ComplexField2D)  # wrap the pinned buffer without a copy
