@@ -641,14 +641,22 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 
   // soft threshold of w (fix-up pass: identity part where the guard fired); x_new -> p
   const float tl = a.tau_l1;
+  if (force) {  // (per plane, so warp-uniform; the main pass never takes it)
+#pragma unroll
+    for (int s = 0; s < SR; ++s)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (force & 1u) rp[s][k].x = v[s][k].x;
+        if (force & 2u) rp[s][k].y = v[s][k].y;
+      }
+  }
   // |x_new| = gsc |w| = gsc n2 rsqrt(n2) feeds the L1 sum with the same rsqrt
 #pragma unroll
   for (int s = 0; s < SR; ++s) {
     float l1 = 0.f;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const float wr = (force & 1u) ? v[s][k].x : rp[s][k].x;
-      const float wi = (force & 2u) ? v[s][k].y : rp[s][k].y;
+      const float wr = rp[s][k].x, wi = rp[s][k].y;
       if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
         p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
         l1 += p[s][k].x;
@@ -657,7 +665,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       const float n2 = fmaf(wr, wr, wi * wi);
       const float r = rsqrt_a(fmaxf(n2, 1e-30f));
       const float shrink = 1.f - tl * r;
-      const float gsc = (tl > 0.f) ? ((n2 > tl * tl) ? shrink : 0.f) : 1.f;
+      // |w| <= tau -> 0 (tau = 0: shrink = 1 for w != 0, and w = 0 maps to 0 either way)
+      const float gsc = (n2 > tl * tl) ? shrink : 0.f;
       p[s][k] = make_float2(wr * gsc, wi * gsc);
       l1 = fmaf(gsc * n2, r, l1);
     }
