@@ -1,7 +1,9 @@
 """Stall-reason totals (and top stalled SASS lines) from an .ncu-rep source page."""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+import os
+k = ["-k", "regex:" + os.environ["NCU_K"]] if os.environ.get("NCU_K") else []  # one kernel of a multi-kernel report
+txt = subprocess.run(["ncu", "-i", rep] + k + ["--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 hdr = rows[1]; ix = {h: i for i, h in enumerate(hdr)}
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
