@@ -583,11 +583,11 @@ struct Engine {
     double sigma2 = (double)geom.nz;  // ||A||^2, closed form (see holo_operator_norm)
     if (cfg.real_nonnegative && (rc = real_opnorm_value(sigma2, s))) return rc;
     for (;;) {
+      ProxArgs a;
+      if ((rc = ensure_prox(a, nzl, geom.ny, geom.nx, cfg.tv_inner_iters, s))) return rc;
       // gradient 2 A^H r_y into scratch (the forward pass below reuses scratch,
       // so a backtracking retry recomputes it)
       if ((rc = adjoint_grad(R, 2.0f, s))) return rc;
-      ProxArgs a;
-      if ((rc = ensure_prox(a, nzl, geom.ny, geom.nx, cfg.tv_inner_iters, s))) return rc;
       a.x = X[sx];
       a.xp = X[sxp];
       a.grad = scratch;
@@ -619,6 +619,9 @@ struct Engine {
         // guard fix-up: planes whose TV output was worse than its input take the
         // identity for that part (prox.py:138-147); rare, so the speculative
         // forward above is simply redone
+        // the speculative forward's row pass overwrote the gradient in
+        // scratch: recompute it (R, the residual spectrum at y, is intact)
+        if ((rc = adjoint_grad(R, 2.0f, s))) return rc;
         do {
           last.guard_fixups += 1;
           ProxArgs f = a;
