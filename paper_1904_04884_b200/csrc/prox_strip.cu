@@ -1,4 +1,4 @@
-// K4 (v4): fused-lasso prox on 64x64 register-strip regions (planes >= 64x64).
+// K4: fused-lasso prox on 64x64 register-strip regions (planes >= 64x64).
 //
 // Semantics are those of prox.py:104-148 (FGP-TV on Re and Im, step 1/(8 tau),
 // replicated edges, per-plane guard) followed by prox.py:83-96 (complex soft
@@ -6,12 +6,15 @@
 // (solver.py:309-310) and the fp64 partial sums the outer loop needs
 // (solver.py:312-318 ip / dx2, solver.py:146-151 penalty, prox.py:138-147 guard).
 //
-// Layout: a CTA owns a 64x64 region = interior tile (64-2H)^2 plus a halo
-// H = T+2 that is recomputed (temporal blocking).  Regions are clamped into
-// the plane, so a region edge is either a true plane edge (where "missing
-// neighbour" is exactly the replicated-edge rule: zero up/left difference,
-// no down/right D^T term) or at least H pixels from every interior pixel
-// (garbage that cannot reach the interior in T+2 steps).  No per-pixel masks.
+// Layout: a CTA owns a 64x64 region = interior tile plus a recomputed halo
+// (temporal blocking: T+1 rows/columns before the tile, T after, rounded
+// even).  Regions are clamped into the plane, so a region edge is either a
+// true plane edge (where "missing neighbour" is exactly the replicated-edge
+// rule: zero up/left difference, no down/right D^T term) or far enough from
+// every interior pixel that its garbage cannot reach it.  No per-pixel masks.
+// The multi-pass kernels (large T) walk column strips instead, taking the rows
+// above a frame from the previous region (see work_geom_walk).  A persistent
+// CTA per SM streams the next region's inputs in by TMA while it works.
 //
 // 512 threads = 16 warps; warp w owns rows 4w..4w+3 of all 64 columns and
 // lane l owns columns 2l, 2l+1, so each thread keeps a 4x2 tile of packed
