@@ -273,6 +273,13 @@ def main():
             nid = torch.tensor(list(buf.raw), dtype=torch.uint8, device=dev)
         dist.broadcast(nid, 0)
         eng = HoloEngine(geom, local, shard=(rank, world, bytes(nid.cpu().tolist())))
+        if world > 1 and os.environ.get("HOLO_PEER_ALLREDUCE") == "1":
+            # forward plane sum over NVLink peer memory instead of the NCCL allreduce
+            def gather(blob):
+                out = [None] * world
+                dist.all_gather_object(out, blob)
+                return out
+            eng.enable_peer_reduction(gather)
     else:
         eng = HoloEngine(geom, local)
     b_dev = torch.as_tensor(b, dtype=torch.float64, device=dev).contiguous()

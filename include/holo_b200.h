@@ -89,6 +89,21 @@ int holo_create_sharded(const holo_geometry* geom, int device, const void* nccl_
  * the collective until every member arrives), each on its own stream.  Destroy
  * every handle with holo_destroy. */
 int holo_create_local_group(const holo_geometry* geom, int device, int nranks, holo_handle** out);
+
+/* Peer-memory reduction of the forward plane sum (replaces the NCCL spectrum
+ * allreduce for a z-sharded handle; no reference counterpart -- the reference
+ * sums planes in one process, solver.py:117-123).  Rank r owns slice
+ * [r*L, (r+1)*L) of the P-element spectrum, L = holo_peer_slice(P, nranks);
+ * one kernel sums the local plane groups and stores each slice into its
+ * owner's inbox over NVLink, a second sums the owner's slice in rank order and
+ * stores it into every rank's result (deterministic).  holo_peer_export writes
+ * this rank's CUDA IPC handles (blob = NULL: *nbytes = blob size); the caller
+ * all-gathers the blobs in rank order and passes them to holo_peer_import,
+ * after which every solve uses the peer path.  The in-process rank group
+ * (holo_create_local_group) uses it by default. */
+int holo_peer_export(holo_handle* h, void* blob, int64_t* nbytes);
+int holo_peer_import(holo_handle* h, const void* blobs, int64_t nbytes_each);
+int64_t holo_peer_slice(int64_t plane_elems, int32_t nranks);
 int holo_destroy(holo_handle* h);
 int holo_local_planes(const holo_handle* h, int32_t* k_begin, int32_t* k_end);
 

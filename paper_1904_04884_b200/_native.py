@@ -62,6 +62,9 @@ SIGNATURES = {
                                            ctypes.POINTER(_H)]),
     "holo_create_local_group": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int,
                                                ctypes.POINTER(_H)]),
+    "holo_peer_export": (ctypes.c_int, [_H, _P, ctypes.POINTER(ctypes.c_int64)]),
+    "holo_peer_import": (ctypes.c_int, [_H, _P, ctypes.c_int64]),
+    "holo_peer_slice": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32]),
     "holo_destroy": (ctypes.c_int, [_H]),
     "holo_local_planes": (ctypes.c_int, [_H, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "holo_operator_norm": (ctypes.c_int, [_H, _I, ctypes.POINTER(_D)]),

@@ -218,6 +218,24 @@ struct LocalGroup {
       if ((e = cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming))) return e;
     return cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
   }
+  // stream barrier across members: every member's stream waits for every
+  // member's work enqueued before the call (events; no kernel waits)
+  cudaError_t barrier(int r, cudaStream_t s) {
+    std::unique_lock<std::mutex> lk(m);
+    cudaError_t e = cudaEventRecord(ev[r], s);
+    if (e) return e;
+    const long long my_gen = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != my_gen; });
+    }
+    for (int i = 0; i < n; ++i)
+      if ((e = cudaStreamWaitEvent(s, ev[i], 0))) return e;
+    return cudaSuccess;
+  }
   // sum over members of buf (count elements of T), in place on every member
   template <class T>
   cudaError_t allreduce(int r, T* b, long long count, cudaStream_t s) {
@@ -260,6 +278,50 @@ struct Engine {
   ncclComm_t comm = nullptr;
 #endif
   std::shared_ptr<LocalGroup> lgroup;  // in-process rank group (tests), else NCCL
+  // peer-memory reduction of the forward spectrum (peer.cu): the rank group
+  // always, NCCL ranks after holo_peer_import
+  bool peer_on = false;
+  PeerSet pset;
+  float2* pr_inbox = nullptr;
+  float2* pr_result = nullptr;
+  unsigned long long* pr_flags = nullptr;
+  unsigned* pr_counter = nullptr;  // [2] threadfence-reduction counters
+  int* pr_err = nullptr;
+  unsigned long long pr_epoch = 0;
+  std::vector<void*> pr_mapped;  // IPC mappings of the other ranks' buffers
+  int ensure_peer_buffers() {
+    if (pr_inbox) return HOLO_OK;
+    const long long L = peer_slice(P, nranks);
+    HOLO_CUDA(cudaMalloc(&pr_inbox, sizeof(float2) * (size_t)nranks * L));
+    HOLO_CUDA(cudaMalloc(&pr_result, sizeof(float2) * (size_t)nranks * L));
+    HOLO_CUDA(cudaMalloc(&pr_flags, sizeof(unsigned long long) * 2 * kMaxPeers));
+    HOLO_CUDA(cudaMalloc(&pr_counter, sizeof(unsigned) * 2));
+    HOLO_CUDA(cudaMalloc(&pr_err, sizeof(int)));
+    HOLO_CUDA(cudaMemset(pr_flags, 0, sizeof(unsigned long long) * 2 * kMaxPeers));
+    HOLO_CUDA(cudaMemset(pr_counter, 0, sizeof(unsigned) * 2));
+    HOLO_CUDA(cudaMemset(pr_err, 0, sizeof(int)));
+    pset.nranks = nranks;
+    pset.rank = rank;
+    pset.L = L;
+    pset.inbox[rank] = pr_inbox;
+    pset.result[rank] = pr_result;
+    pset.flags[rank] = pr_flags;
+    return HOLO_OK;
+  }
+  // S_out = sum over ranks of sum over plane groups of Spart (replaces
+  // sum_groups + the spectrum allreduce)
+  int peer_reduce(float2* S_out, cudaStream_t s) {
+    const unsigned long long e = ++pr_epoch;
+    const long long max_polls = 1LL << 26;  // ~20 s: a dead peer fails instead of hanging
+    HOLO_CUDA(peer_scatter(Spart, groups, P, pset, e, pr_counter, s));
+    if (lgroup) HOLO_CUDA(lgroup->barrier(rank, s));  // one GPU: no kernel may wait on another rank's
+    HOLO_CUDA(peer_wait(pset, 0, e, max_polls, pr_err, s));
+    HOLO_CUDA(peer_gather(P, pset, e, pr_counter + 1, s));
+    if (lgroup) HOLO_CUDA(lgroup->barrier(rank, s));
+    HOLO_CUDA(peer_wait(pset, 1, e, max_polls, pr_err, s));
+    HOLO_CUDA(cudaMemcpyAsync(S_out, pr_result, sizeof(float2) * (size_t)P, cudaMemcpyDeviceToDevice, s));
+    return HOLO_OK;
+  }
   // volume buffers
   float2* X[3] = {nullptr, nullptr, nullptr};
   float2* scratch = nullptr;
@@ -326,6 +388,9 @@ struct Engine {
       stage_ev[i] = nullptr;
     }
     cudaFree(mp_v); cudaFree(mp_s); cudaFree(mp_r); cudaFree(mp_tvv);
+    for (void* m : pr_mapped) cudaIpcCloseMemHandle(m);
+    pr_mapped.clear();
+    cudaFree(pr_inbox); cudaFree(pr_result); cudaFree(pr_flags); cudaFree(pr_counter); cudaFree(pr_err);
     plan_free(plan);
 #ifdef HOLO_WITH_NCCL
     if (comm) ncclCommDestroy(comm);
@@ -476,6 +541,12 @@ struct Engine {
   int forward_spectrum(const float2* x, float2* S_out, cudaStream_t s) {
     PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzl * geom.ny, false, 1.0f, s));
     PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzl, kb, groups, s));
+    if (peer_on && nranks > 1) {  // fused group sum + reduce-scatter + all-gather over peer memory
+      HOLO_CUDA(prof.begin(PK_SUM_GROUPS, s));
+      int rc = peer_reduce(S_out, s);
+      HOLO_CUDA(prof.end(s));
+      return rc;
+    }
     PROF(PK_SUM_GROUPS, s, sum_groups(plan, Spart, groups, S_out, s));
     return allreduce_spec(S_out, s);
   }
@@ -501,7 +572,10 @@ struct Engine {
 
   int read_scalars(cudaStream_t s) {
     HOLO_CUDA(cudaMemcpyAsync(h_scal, scal, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, s));
+    int perr = 0;
+    if (peer_on) HOLO_CUDA(cudaMemcpyAsync(&perr, pr_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HOLO_CUDA(cudaStreamSynchronize(s));
+    if (perr) return fail(HOLO_ERR_NCCL, "peer spectrum reduction: a rank did not arrive (timeout)");
     HOLO_CUDA(prof.harvest());
     return HOLO_OK;
   }
@@ -920,8 +994,81 @@ int holo_create_local_group(const holo_geometry* geom, int device, int nranks, h
       h->e.lgroup = grp;
       out[r] = h;
     }
+    // the rank group reduces the forward spectrum through the peer kernels
+    // (its members' buffers are plain pointers on this device)
+    for (int r = 0; r < nranks && nranks > 1; ++r) {
+      int rc = out[r]->e.ensure_peer_buffers();
+      if (rc) return rc;
+    }
+    for (int r = 0; r < nranks && nranks > 1; ++r) {
+      auto& e = out[r]->e;
+      for (int j = 0; j < nranks; ++j) {
+        e.pset.inbox[j] = out[j]->e.pr_inbox;
+        e.pset.result[j] = out[j]->e.pr_result;
+        e.pset.flags[j] = out[j]->e.pr_flags;
+      }
+      e.peer_on = true;
+    }
     return HOLO_OK;
   })
+}
+
+int holo_peer_export(holo_handle* h, void* blob, int64_t* nbytes) {
+  GUARD_HANDLE(h);
+  if (!nbytes) return fail(HOLO_ERR_INVALID, "null argument");
+  constexpr int64_t kBlob = 3 * (int64_t)sizeof(cudaIpcMemHandle_t) + 8;
+  if (!blob) {
+    *nbytes = kBlob;
+    return HOLO_OK;
+  }
+  if (*nbytes < kBlob) return fail(HOLO_ERR_INVALID, "peer blob buffer too small");
+  TRY({
+    auto& e = h->e;
+    if (e.nranks < 2 || e.nranks > holo::kMaxPeers) return fail(HOLO_ERR_INVALID, "peer reduction needs 2..8 ranks");
+    if (int rc = e.ensure_peer_buffers()) return rc;
+    cudaIpcMemHandle_t hd[3];
+    HOLO_CUDA(cudaIpcGetMemHandle(&hd[0], e.pr_inbox));
+    HOLO_CUDA(cudaIpcGetMemHandle(&hd[1], e.pr_result));
+    HOLO_CUDA(cudaIpcGetMemHandle(&hd[2], e.pr_flags));
+    std::memcpy(blob, hd, sizeof(hd));
+    const int64_t L = e.pset.L;
+    std::memcpy(static_cast<char*>(blob) + sizeof(hd), &L, 8);
+    *nbytes = kBlob;
+    return HOLO_OK;
+  })
+}
+
+int holo_peer_import(holo_handle* h, const void* blobs, int64_t nbytes_each) {
+  GUARD_HANDLE(h);
+  if (!blobs) return fail(HOLO_ERR_INVALID, "null argument");
+  TRY({
+    auto& e = h->e;
+    if (!e.pr_inbox) return fail(HOLO_ERR_INVALID, "holo_peer_export first");
+    cudaIpcMemHandle_t hd[3];
+    if (nbytes_each < (int64_t)sizeof(hd) + 8) return fail(HOLO_ERR_INVALID, "bad peer blob size");
+    for (int j = 0; j < e.nranks; ++j) {
+      if (j == e.rank) continue;
+      const char* b = static_cast<const char*>(blobs) + (size_t)j * nbytes_each;
+      int64_t L = 0;
+      std::memcpy(hd, b, sizeof(hd));
+      std::memcpy(&L, b + sizeof(hd), 8);
+      if (L != e.pset.L) return fail(HOLO_ERR_INVALID, "peer slice length mismatch (different geometry?)");
+      void* p[3];
+      for (int k = 0; k < 3; ++k) {
+        HOLO_CUDA(cudaIpcOpenMemHandle(&p[k], hd[k], cudaIpcMemLazyEnablePeerAccess));
+        e.pr_mapped.push_back(p[k]);
+      }
+      e.pset.inbox[j] = static_cast<float2*>(p[0]);
+      e.pset.result[j] = static_cast<float2*>(p[1]);
+      e.pset.flags[j] = static_cast<unsigned long long*>(p[2]);
+    }
+    e.peer_on = true;
+    return HOLO_OK;
+  })
+}
+
+int64_t holo_peer_slice(int64_t plane_elems, int32_t nranks) {
+  return nranks >= 1 ? holo::peer_slice(plane_elems, nranks) : 0;
 }
 
 int holo_destroy(holo_handle* h) {

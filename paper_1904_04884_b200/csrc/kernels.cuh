@@ -61,6 +61,22 @@ struct ProxArgs {
   float* tvv = nullptr;              // per-tile TV(v) partials [tile][2], first pass -> last pass
 };
 
+// Peer-memory spectrum reduction (peer.cu): every rank's symmetric buffers.
+constexpr int kMaxPeers = 8;
+struct PeerSet {
+  float2* inbox[kMaxPeers] = {};               // [nranks][L]
+  float2* result[kMaxPeers] = {};              // [nranks * L]
+  unsigned long long* flags[kMaxPeers] = {};   // [2][kMaxPeers] epoch counters
+  int nranks = 0, rank = 0;
+  long long L = 0;                             // slice length, nranks * L >= P
+};
+long long peer_slice(long long P, int nranks);
+cudaError_t peer_scatter(const float2* Spart, int groups, long long P, const PeerSet& ps, unsigned long long epoch,
+                         unsigned* counter, cudaStream_t s);
+cudaError_t peer_wait(const PeerSet& ps, int which, unsigned long long epoch, long long max_polls, int* err,
+                      cudaStream_t s);
+cudaError_t peer_gather(long long P, const PeerSet& ps, unsigned long long epoch, unsigned* counter, cudaStream_t s);
+
 // 2D tiled TMA descriptor over float rows (kernels.cu); nonzero on failure
 int encode_tiled_2d(CUtensorMap* m, const void* base, long long inner, long long rows, int box_inner, int box_rows);
 bool plan_supported(int nx, int ny);

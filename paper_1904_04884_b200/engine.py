@@ -53,6 +53,20 @@ class HoloEngine:
         nat.check(self.lib.holo_local_planes(h, ctypes.byref(kb), ctypes.byref(ke)))
         self.k_begin, self.k_end = kb.value, ke.value
 
+    def enable_peer_reduction(self, all_gather_bytes):
+        """Switch this z-shard's forward-spectrum allreduce from NCCL to the
+        peer-memory kernels (holo_peer_export / holo_peer_import).
+        ``all_gather_bytes(blob) -> list[bytes]`` returns every rank's blob in
+        rank order (e.g. torch.distributed.all_gather_object)."""
+        n = ctypes.c_int64()
+        nat.check(self.lib.holo_peer_export(self.h, None, ctypes.byref(n)), "holo_peer_export")
+        buf = ctypes.create_string_buffer(n.value)
+        nat.check(self.lib.holo_peer_export(self.h, buf, ctypes.byref(n)), "holo_peer_export")
+        blobs = all_gather_bytes(buf.raw[: n.value])
+        assert all(len(b) == n.value for b in blobs)
+        allb = ctypes.create_string_buffer(b"".join(blobs), n.value * len(blobs))
+        nat.check(self.lib.holo_peer_import(self.h, allb, n.value), "holo_peer_import")
+
     @classmethod
     def local_group(cls, geom, nranks: int, device: int | None = None) -> list["HoloEngine"]:
         """``nranks`` z-shards of one geometry on ONE GPU whose two collectives

@@ -134,3 +134,78 @@ def test_plane_ranges_partition():
             rs = [plane_range(nz, r, n) for r in range(n)]
             assert rs[0][0] == 0 and rs[-1][1] == nz
             assert all(rs[i][1] == rs[i + 1][0] for i in range(n - 1))
+
+
+# ---- peer-memory spectrum reduction (csrc/peer.cu): host-side algorithm ----
+
+def _peer_reduce_model(rank, world, port, q, P, groups, seed):
+    """Rank r models holo_peer_*: k_peer_scatter sums its plane groups (fp32,
+    group order) and sends element i to owner i // L, slot r; k_peer_gather
+    sums the owner's slots in rank order (fp32) and all-gathers.  The exchange
+    is all_gather over gloo (what the IPC stores deliver)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_04884_b200 import _native as nat
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L = nat.load().holo_peer_slice(P, world)
+    rng = np.random.default_rng(seed + rank)
+    spart = (rng.standard_normal((groups, P)) + 1j * rng.standard_normal((groups, P))).astype(np.complex64)
+    part = spart[0].copy()
+    for g in range(1, groups):
+        part = (part + spart[g]).astype(np.complex64)
+    # scatter: my partial of every owner's slice, padded to world * L
+    padded = np.zeros(world * L, np.complex64)
+    padded[:P] = part
+    mine = [None] * world
+    dist.all_gather_object(mine, padded.reshape(world, L))  # row o of rank j = rank j's partial of slice o
+    inbox = np.stack([mine[j][rank] for j in range(world)])  # [slot j][L], as k_peer_scatter writes it
+    red = inbox[0].copy()
+    for j in range(1, world):
+        red = (red + inbox[j]).astype(np.complex64)
+    slices = [None] * world
+    dist.all_gather_object(slices, red)
+    result = np.concatenate(slices)[:P]
+    q.put((rank, part, result))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,P,groups", [(2, 4096, 3), (3, 1000, 2), (4, 65536, 5)])
+def test_peer_reduction_model(world, P, groups):
+    """Slice ownership covers every element once, the rank-order fp32 sums are
+    deterministic, and every rank ends with the same spectrum = sum over ranks
+    of sum over groups."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_reduce_model, args=(r, world, port, q, P, groups, 11)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (part, res)) for r, part, res in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = [out[r][0] for r in range(world)]
+    expect = parts[0].copy()
+    for r in range(1, world):
+        expect = (expect + parts[r]).astype(np.complex64)
+    for r in range(world):
+        assert np.array_equal(out[r][1], expect)  # bitwise: rank-order fp32 sums
+
+
+def test_peer_slices_cover_the_plane():
+    from paper_1904_04884_b200 import _native as nat
+    lib = nat.load()
+    for P in (64, 1000, 65536, 1 << 20, 1 << 22):
+        for n in range(1, 9):
+            L = lib.holo_peer_slice(P, n)
+            assert L % 64 == 0 and n * L >= P and (n * L - P) < 64 * n + L
+            owners = np.minimum(np.arange(P) // L, n - 1)
+            assert owners.max() < n and np.all(np.arange(P) // L < n)
