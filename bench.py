@@ -395,7 +395,15 @@ def main():
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_voxel": KERNEL_BYTES[dom]},
             "step_roofline": {"bytes_per_voxel_iter": BYTES_PER_VOXEL_ITER, "achieved": step_roof, "peak": hbm,
-                              "frac": step_roof / hbm},
+                              "frac": step_roof / hbm, "frac_of_spec_8tbs": step_roof / 8000.0,
+                              # compulsory floor (x, x_prev read, x_new write) and the
+                              # radix-2 flop model F = 10 log2(P) + 48 T + 100 against the spec FP32 peak
+                              "floor_bytes_per_voxel_iter": 24,
+                              "floor_frac": value / world * 24 / 1e9 / hbm,
+                              "flop_per_voxel_iter": 10 * math.log2(nx * ny) + 48 * inner + 100,
+                              "fp32_tflops": value / world * (10 * math.log2(nx * ny) + 48 * inner + 100) / 1e12,
+                              "fp32_peak_tflops": 74.4,
+                              "fp32_frac": value / world * (10 * math.log2(nx * ny) + 48 * inner + 100) / 74.4e12},
             "kernels_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "kernel_share": {k: round(v["ms"] / total_kernel_ms, 4) for k, v in prof.items()} if total_kernel_ms else {},
             "gpu_launches": int(launches),
