@@ -358,7 +358,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   auto top_rule = [&]() { return EDGE && w == 0 && (!WALK || top); };
 
   float2 v[SR][2], p[SR][2], q[SR][2], rp[SR][2], rq[SR][2];
-  if (TV && PH == 1) fetch_above(1, 0);  // v above the frame, read by iteration 0
+  if (TV && PH == 1) fetch_above(0, 0);  // v above the frame, read by iteration 0
   // PH: pass kind of a multi-pass FGP (compile-time, so no kernel carries the
   // state handling it does not use): 0 single pass, 1 first, 2 middle, 3 last
   constexpr bool first = PH == 0 || PH == 1, last = PH == 0 || PH == 3;
@@ -437,6 +437,41 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   const float2 mtau = splat2(-a.tau_tv);
   const float ttv = a.tau_tv;
 
+  // soft threshold of w (fix-up pass: identity part where the guard fired); x_new -> p
+  auto soft_rows = [&]() {
+  const float tl = a.tau_l1;
+  if (force) {  // (per plane, so warp-uniform; the main pass never takes it)
+#pragma unroll
+    for (int s = 0; s < SR; ++s)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (force & 1u) rp[s][k].x = v[s][k].x;
+        if (force & 2u) rp[s][k].y = v[s][k].y;
+      }
+  }
+  // |x_new| = gsc |w| = gsc n2 rsqrt(n2) feeds the L1 sum with the same rsqrt
+#pragma unroll
+  for (int s = 0; s < SR; ++s) {
+    float l1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float wr = rp[s][k].x, wi = rp[s][k].y;
+      if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
+        p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
+        l1 += p[s][k].x;
+        continue;
+      }
+      const float n2 = fmaf(wr, wr, wi * wi);
+      const float r = rsqrt_a(fmaxf(n2, 1e-30f));
+      const float shrink = 1.f - tl * r;
+      // |w| <= tau -> 0 (tau = 0: shrink = 1 for w != 0, and w = 0 maps to 0 either way)
+      const float gsc = (n2 > tl * tl) ? shrink : 0.f;
+      p[s][k] = make_float2(wr * gsc, wi * gsc);
+      l1 = fmaf(gsc * n2, r, l1);
+    }
+    if (rInt & (1u << s)) acc[PT_L1] += l1;
+  }
+  };
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
     // X = v - tau (rp + rq - rq_right) of the band's last row: the last-row u
@@ -455,14 +490,14 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     const int tstart = first ? 1 : a.t0;
     if (first) {
     // ---- iteration 0: r = 0, u = v, beta_0 = 0; TV(v) for the guard ----
-    sm.bot[1][w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
+    sm.bot[0][w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     save_rows(0, v);
     __syncthreads();
     if constexpr (WALK) {  // every thread has read this region's x_prev: stream the next region's in
       if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
     }
     {
-      float2 up0 = above_of(1, 0, v[0][0]), up1 = above_of(1, 1, v[0][1]);
+      float2 up0 = above_of(0, 0, v[0][0]), up1 = above_of(0, 1, v[0][1]);
 #pragma unroll
       for (int s = 0; s < SR; ++s) {
         float2 gx0, gx1;
@@ -492,8 +527,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       }
     }
     }
-    // publish for the first sweep (iteration t reads buffer (t-1)&1, writes t&1)
-    int lastbuf = first ? 0 : (a.t0 - 1) & 1;
+    // publish for the first sweep (iteration t reads buffer t&1, writes its
+    // complement; iteration 0 used bot[0], so the first sweep reads buffer 1)
+    int lastbuf = first ? 1 : a.t0 & 1;
     {
       xlast(xl0, xl1);
       sm.top[lastbuf][w][lane] = f4(rp[0][0], rp[0][1]);
@@ -509,7 +545,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     const float2 ptau = splat2(a.tau_tv);
 #pragma unroll 2
     for (int t = tstart; t < a.t1; ++t) {
-      const int b = (t - 1) & 1;  // buffers holding this iteration's band-top rp / band-bottom X
+      const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
       // one row's dual update from its u, given the u of the row above
       auto update = [&](int s, float2 u0, float2 u1, float2 up0, float2 up1) {
@@ -596,7 +632,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       return;  // every band read of this region precedes the last sweep's barrier
     }
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
-    const int bf = a.inner & 1;  // not read by the last sweep
+    const int bf = lastbuf ^ 1;  // read by the last sweep, which every band has finished
     sm.top[bf][w][lane] = f4(p[0][0], p[0][1]);
     __syncthreads();
     {
@@ -613,6 +649,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     sm.bot[0][w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);  // bot last read by the final sweep, a sync ago
     save_rows(kSaveW, rp);
     fetch_above(0, kSaveW);
+    soft_rows();  // x_new -> p: needs only this band's w, so it runs ahead of the barrier
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
@@ -633,57 +670,28 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         }
       }
     }
-    __syncthreads();  // bot reads done before x_new is published
   } else {
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
       rp[s][0] = v[s][0];
       rp[s][1] = v[s][1];
     }
+    soft_rows();
   }
+  // x_new exchange: bot[1] after the FGP (the guard's reads of bot[0] may
+  // still be running; the next region's first band-slot write, iteration 0's,
+  // goes to bot[0] and its first-sweep publication follows a CTA barrier)
+  constexpr int xb = TV ? 1 : 0;
 
-  // soft threshold of w (fix-up pass: identity part where the guard fired); x_new -> p
-  const float tl = a.tau_l1;
-  if (force) {  // (per plane, so warp-uniform; the main pass never takes it)
-#pragma unroll
-    for (int s = 0; s < SR; ++s)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (force & 1u) rp[s][k].x = v[s][k].x;
-        if (force & 2u) rp[s][k].y = v[s][k].y;
-      }
-  }
-  // |x_new| = gsc |w| = gsc n2 rsqrt(n2) feeds the L1 sum with the same rsqrt
-#pragma unroll
-  for (int s = 0; s < SR; ++s) {
-    float l1 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const float wr = rp[s][k].x, wi = rp[s][k].y;
-      if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
-        p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
-        l1 += p[s][k].x;
-        continue;
-      }
-      const float n2 = fmaf(wr, wr, wi * wi);
-      const float r = rsqrt_a(fmaxf(n2, 1e-30f));
-      const float shrink = 1.f - tl * r;
-      // |w| <= tau -> 0 (tau = 0: shrink = 1 for w != 0, and w = 0 maps to 0 either way)
-      const float gsc = (n2 > tl * tl) ? shrink : 0.f;
-      p[s][k] = make_float2(wr * gsc, wi * gsc);
-      l1 = fmaf(gsc * n2, r, l1);
-    }
-    if (rInt & (1u << s)) acc[PT_L1] += l1;
-  }
-  sm.bot[0][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+  sm.bot[xb][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
   save_rows(kSaveX, p);
-  fetch_above(0, kSaveX);
+  fetch_above(xb, kSaveX);
   __syncthreads();
   if constexpr (WALK && !TV) {  // (TV: issued after iteration 0's barrier)
     if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
   }
   {
-    float2 up0 = above_of(0, 0, p[0][0]), up1 = above_of(0, 1, p[0][1]);
+    float2 up0 = above_of(xb, 0, p[0][0]), up1 = above_of(xb, 1, p[0][1]);
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta);
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
@@ -760,7 +768,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   // when the epilogue read the slot (evaluated backtracking test), wait for
   // every warp first.  Band slots and geo[] are only rewritten behind the next
   // region's own barriers.
-  if (a.ipdx) __syncthreads();
+  // (no TV: the next region's only exchange writes bot[0] before its barrier)
+  if (!TV || a.ipdx) __syncthreads();
 }
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
