@@ -546,7 +546,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 #pragma unroll 2
     for (int t = tstart; t < a.t1; ++t) {
       const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
-      const float2 bt2 = splat2(__ldg(a.fgp_beta + t));
+      // single pass (T <= 8): the momentum schedule from the parameter bank
+      const float2 bt2 = splat2(PH == 0 ? a.fgpb[t] : __ldg(a.fgp_beta + t));
       // one row's dual update from its u, given the u of the row above
       auto update = [&](int s, float2 u0, float2 u1, float2 up0, float2 up1) {
         float2 gx0, gx1;
