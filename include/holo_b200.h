@@ -181,6 +181,10 @@ int holo_background(const double* images, int32_t T, int32_t ny, int32_t nx, int
 /* ---- instrumentation ---- */
 /* per-kernel-class device time (CUDA events on the launching stream) */
 int holo_profile_enable(holo_handle* h, int32_t on);
+/* record only the classes whose bit is set in mask (bit k = k-th class of
+ * holo_profile_read; default all): timing one class keeps the others' event
+ * records out of a timed region */
+int holo_profile_classes(holo_handle* h, uint32_t mask);
 /* n = #classes; names: n x 32 bytes; ms: accumulated device ms; counts: launches */
 int holo_profile_read(holo_handle* h, int32_t* n, char* names, double* ms, int64_t* counts);
 /* kernels launched by this library since it was loaded (all handles) */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "holo_background": (ctypes.c_int, [_P, _I, _I, _I, _I, _P, _P]),
     "holo_profile_enable": (ctypes.c_int, [_H, _I]),
     "holo_profile_read": (ctypes.c_int, [_H, ctypes.POINTER(_I), _P, _P, _P]),
+    "holo_profile_classes": (ctypes.c_int, [_H, ctypes.c_uint32]),
     "holo_launch_count": (ctypes.c_int64, []),
 }
 

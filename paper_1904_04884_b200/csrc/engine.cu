@@ -120,6 +120,8 @@ static const char* kProfNames[PK_N] = {"adj_cols", "adj_rows", "prox", "fwd_rows
 
 struct Prof {
   bool on = false;
+  unsigned mask = ~0u;  // classes that record (holo_profile_classes)
+  bool cur = false;     // the open begin() recorded
   std::vector<cudaEvent_t> ev;
   std::vector<int> kind;
   int used = 0;
@@ -129,7 +131,8 @@ struct Prof {
     for (int i = 0; i < PK_N; ++i) { ms[i] = 0; cnt[i] = 0; }
   }
   cudaError_t begin(int k, cudaStream_t s) {
-    if (!on) return cudaSuccess;
+    cur = on && ((mask >> k) & 1u);
+    if (!cur) return cudaSuccess;
     if ((int)kind.size() <= used) {
       cudaEvent_t a, b;
       cudaError_t e;
@@ -143,7 +146,8 @@ struct Prof {
     return cudaEventRecord(ev[2 * used], s);
   }
   cudaError_t end(cudaStream_t s) {
-    if (!on) return cudaSuccess;
+    if (!cur) return cudaSuccess;
+    cur = false;
     cudaError_t e = cudaEventRecord(ev[2 * used + 1], s);
     ++used;
     return e;
@@ -1340,6 +1344,12 @@ int holo_profile_enable(holo_handle* h, int32_t on) {
   if (!h) return fail(HOLO_ERR_INVALID, "null handle");
   h->e.prof.on = on != 0;
   h->e.prof.reset();
+  return HOLO_OK;
+}
+
+int holo_profile_classes(holo_handle* h, uint32_t mask) {
+  if (!h) return fail(HOLO_ERR_INVALID, "null handle");
+  h->e.prof.mask = mask;
   return HOLO_OK;
 }
 
