@@ -34,10 +34,10 @@ struct DefaultE {
 template <int N, int EE = DefaultE<N>::value>
 struct FftShape {
   static_assert(N >= 8 && N <= 4096 && (N & (N - 1)) == 0, "N must be a power of two in [8, 4096]");
-  static_assert(EE <= N && (EE == 8 || EE == 16 || EE == 32 || EE == N), "E must be 8, 16 or 32");
+  static_assert(EE <= N && (EE == 8 || EE == 16 || EE == 32 || EE == 64 || EE == N), "E must be 8, 16, 32 or 64");
   static constexpr int E = EE;
   static constexpr int TPF = N / E;
-  static constexpr int SH = E == 32 ? 5 : E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;  // log2 E
+  static constexpr int SH = E == 64 ? 6 : E == 32 ? 5 : E == 16 ? 4 : E == 8 ? 3 : E == 4 ? 2 : 1;  // log2 E  // log2 E
   // padded line length in elements; the +2/+TPF term staggers consecutive
   // lines across banks (lines of one warp start on distinct banks)
   static constexpr int PADN = N + N / E + (TPF >= 16 ? 2 : TPF);
@@ -139,6 +139,25 @@ template <bool INV, int e>
 HD float2 rot16(float2 x) {
   return rot32<INV, 2 * e>(x);
 }
+// cos / sin of pi k / 32, k = 0..31 (fp32-rounded)
+struct Trig64 {
+  static constexpr float c[32] = {1.0f, 0.9951847195625305f, 0.9807852506637573f, 0.9569403529167175f, 0.9238795042037964f, 0.8819212913513184f, 0.8314695954322815f, 0.7730104327201843f, 0.7071067690849304f, 0.6343932747840881f, 0.5555702447891235f, 0.4713967442512512f, 0.3826834261417389f, 0.290284663438797f, 0.19509032368659973f, 0.0980171412229538f, 6.123234262925839e-17f, -0.0980171412229538f, -0.19509032368659973f, -0.290284663438797f, -0.3826834261417389f, -0.4713967442512512f, -0.5555702447891235f, -0.6343932747840881f, -0.7071067690849304f, -0.7730104327201843f, -0.8314695954322815f, -0.8819212913513184f, -0.9238795042037964f, -0.9569403529167175f, -0.9807852506637573f, -0.9951847195625305f};
+  static constexpr float s[32] = {0.0f, 0.0980171412229538f, 0.19509032368659973f, 0.290284663438797f, 0.3826834261417389f, 0.4713967442512512f, 0.5555702447891235f, 0.6343932747840881f, 0.7071067690849304f, 0.7730104327201843f, 0.8314695954322815f, 0.8819212913513184f, 0.9238795042037964f, 0.9569403529167175f, 0.9807852506637573f, 0.9951847195625305f, 1.0f, 0.9951847195625305f, 0.9807852506637573f, 0.9569403529167175f, 0.9238795042037964f, 0.8819212913513184f, 0.8314695954322815f, 0.7730104327201843f, 0.7071067690849304f, 0.6343932747840881f, 0.5555702447891235f, 0.4713967442512512f, 0.3826834261417389f, 0.290284663438797f, 0.19509032368659973f, 0.0980171412229538f};
+};
+// x * exp(-/+ 2 pi i e / 64), e compile-time
+template <bool INV, int e>
+HD float2 rot64(float2 x) {
+  constexpr int ee = e & 63;
+  if constexpr ((ee & 1) == 0) {
+    return rot32<INV, ee / 2>(x);
+  } else {
+    constexpr int h = ee & 31;
+    constexpr float cs = (ee < 32) ? Trig64::c[h] : -Trig64::c[h];
+    constexpr float sn = (ee < 32) ? Trig64::s[h] : -Trig64::s[h];
+    constexpr float s = INV ? sn : -sn;
+    return fma2(swp(x), make_float2(-s, s), mul2(x, make_float2(cs, cs)));
+  }
+}
 
 // a * w (forward) or a * conj(w) (inverse) with the table entry t = (w, conj w):
 //   a w      = a.x (w)      + a.y swap(conj w)
@@ -227,6 +246,30 @@ struct Dft<32, INV> {
   }
 };
 
+// 64 = 2 x 32: DFT32 of the even and odd samples, X[k] = E[k] +- w64^k O[k].
+template <bool INV>
+struct Dft<64, INV> {
+  template <int K>
+  static HD void combine(float2 (&ev)[32], float2 (&od)[32], float2 (&a)[64]) {
+    if constexpr (K < 32) {
+      const float2 o = rot64<INV, K>(od[K]);
+      a[K] = add2(ev[K], o);
+      a[K + 32] = sub2(ev[K], o);
+      combine<K + 1>(ev, od, a);
+    }
+  }
+  static HD void run(float2 (&a)[64]) {
+    float2 ev[32], od[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      ev[i] = a[2 * i];
+      od[i] = a[2 * i + 1];
+    }
+    Dft<32, INV>::run(ev);
+    Dft<32, INV>::run(od);
+    combine<0>(ev, od, a);
+  }
+};
 // One Stockham pass of radix R with NS = product of earlier radices.
 template <int N, int E, int R, int NS, bool INV, bool FIRST, bool LAST>
 HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __restrict__ tw) {

@@ -32,6 +32,9 @@ namespace holo {
 namespace {
 
 constexpr int kRowThreads = 256;
+// row-pass CTA size: 4 rows of 64-element threads (2 CTAs per SM by shared memory)
+template <int E>
+constexpr int row_threads() { return E == 64 ? 128 : kRowThreads; }
 
 template <class F>
 bool dispatch_n(int n, F&& f) {
@@ -52,14 +55,17 @@ bool dispatch_n(int n, F&& f) {
 
 inline int col_width(int ny) { return ny >= 4096 ? 4 : 8; }
 
+#ifndef HOLO_ROW_E64_N
+#define HOLO_ROW_E64_N 2048  // 2048-point rows: 64 x 32, one exchange instead of two
+#endif
 // elements per thread: 32 (one shared-memory exchange per 1024-point line)
 // where registers allow; the accumulating forward column pass keeps 16
 template <int N>
 struct EBig {
-  static constexpr int value = N >= 512 ? 32 : DefaultE<N>::value;
+  static constexpr int value = N == HOLO_ROW_E64_N ? 64 : N >= 512 ? 32 : DefaultE<N>::value;
 };
 template <int E>
-constexpr int tw_slot() { return E == 32 ? 1 : 0; }
+constexpr int tw_slot() { return E >= 32 ? 1 : 0; }
 
 // ------------------------------------------------------------ K1 tables ----
 
@@ -124,11 +130,11 @@ __global__ void k_phase(uint64_t* tab, uint8_t* mask, int ny, int nx, double pit
 // ------------------------------------------------------------- K3 rows -----
 
 template <int N, bool INV, int E_>
-__global__ void __launch_bounds__(kRowThreads) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
+__global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
                                                           long long nrows, float scale, const float4* __restrict__ twg) {
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
-  constexpr int RPC = kRowThreads / TPF;
+  constexpr int RPC = row_threads<E_>() / TPF;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* buf = smem + 2 * N;
@@ -1013,16 +1019,17 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
     constexpr int N = decltype(nc)::value;
     constexpr int E = EBig<N>::value;
     using Sh = FftShape<N, E>;
-    constexpr int RPC = kRowThreads / Sh::TPF;
+    constexpr int NT = row_threads<E>();
+    constexpr int RPC = NT / Sh::TPF;
     const size_t smem = sizeof(float2) * (2 * N + (size_t)RPC * Sh::PADN);
     const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
     if (inverse) {
       err = set_smem(k_fft_rows<N, true, E>, smem);
-      k_fft_rows<N, true, E><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
+      k_fft_rows<N, true, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
   COUNT_LAUNCH(1);
     } else {
       err = set_smem(k_fft_rows<N, false, E>, smem);
-      k_fft_rows<N, false, E><<<grid, kRowThreads, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
+      k_fft_rows<N, false, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
   COUNT_LAUNCH(1);
     }
   });
