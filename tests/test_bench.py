@@ -26,3 +26,14 @@ def test_reference_arm_json_contract():
     assert d["e2e"] == {"value": d["value"], "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("c1: 256x256x64")
+
+
+def test_reference_arm_non_zero_rank_is_silent():
+    """Under torchrun (N > 1) only rank 0 runs the CPU reference; the other
+    ranks exit 0 without work or output."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", RANK="1", LOCAL_RANK="1", WORLD_SIZE="2")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=120,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
