@@ -5,10 +5,12 @@
 
 One step = one complete fista() solve of the config (100 FISTA iterations on
 a synthetic hologram whose inputs are already resident in HBM).  N>1 runs are
-launched by torchrun; the volume is z-sharded over the ranks (weak scaling
-would fix planes/GPU; here the C3 volume is fixed, so scaling is "strong").
-The reference arm (--impl reference) times the CPU oracle port on the box's
-host cores on a bounded sample of the same workload.
+launched by torchrun (`--gpus N` without torchrun relaunches itself under
+it); the volume is z-sharded over the ranks (weak scaling would fix
+planes/GPU; here the C3 volume is fixed, so scaling is "strong").
+The reference arm (--impl reference) times the reference's own CPU solver
+(holotrack from baseline/_ref; the oracle port if that install is absent)
+on every host core, on a bounded sample of the same workload and hologram.
 """
 
 from __future__ import annotations
@@ -147,54 +149,112 @@ def peaks():
 
 
 # ------------------------------------------------------------- CPU arms ----
+#
+# The CPU legs time the reference itself when the driver's offline install of
+# the unmodified package is present (baseline/_ref/holotrack, the
+# `pip install --no-deps --target baseline/_ref /root/reference/pkg` of
+# DESIGN.md section 6), else the oracle port (pinned to the reference by
+# tests/test_oracle.py).  Sample: the config's full lateral size, the
+# first REF_PLANES planes, REF_ITERS iterations from x = 0 (the second is a
+# steady-state iteration: momentum on, y != 0, every plane forward-projected),
+# initial step 1/(2 nz) so the infeasible power iteration is skipped; the
+# per-voxel cost is independent of nz.
+
+REF_PLANES, REF_ITERS = 4, 2
+
+
+def reference_module():
+    """holotrack.solver from baseline/_ref (driver install), or None."""
+    for base in (os.path.join(ROOT, "baseline", "_ref"), os.path.join(ROOT, "baseline", "_ref", "pkg", "src")):
+        if os.path.isfile(os.path.join(base, "holotrack", "solver.py")):
+            if base not in sys.path:
+                sys.path.insert(0, base)
+            import holotrack.solver as hs
+            return hs
+    return None
+
 
 def _cpu_sample(args):
-    b, nx, ny, nzs, iters, lam_l1, lam_tv, inner = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    """One bounded CPU solve of the sample; returns (voxel-iterations, seconds,
+    dense volume or None, history)."""
+    b, nx, ny, nzs, iters, lam_l1, lam_tv, inner, want_x = args
+    hs = reference_module()
+    step = 1.0 / (2.0 * nzs)
+    if hs is not None:  # the unmodified reference, through its public API
+        from holotrack.optics import ComplexField2D, VolumeGeometry
+        from holotrack.prox import RegularizerWeights
+        g = VolumeGeometry(nx, ny, nzs, PITCH, DZ, Z0, LAM)
+        cfg = hs.SolverConfig(weights=RegularizerWeights(lam_l1, lam_tv), max_iters=iters, tv_inner_iters=inner,
+                              step_size=step)
+        t0 = time.perf_counter()
+        vol, rep = hs.fista(ComplexField2D(b, PITCH, LAM), g, cfg)
+        dt = time.perf_counter() - t0
+        return nx * ny * nzs * rep.iterations, dt, (vol.to_dense() if want_x else None), list(rep.objective)
     from oracle.holo_oracle import Geometry, fista_solve
     g = Geometry(nx, ny, nzs, PITCH, DZ, Z0, LAM)
     t0 = time.perf_counter()
-    res = fista_solve(b, g, lam_l1=lam_l1, lam_tv=lam_tv, max_iters=iters, inner=inner,
-                      step_size=1.0 / (2.0 * nzs))
+    res = fista_solve(b, g, lam_l1=lam_l1, lam_tv=lam_tv, max_iters=iters, inner=inner, step_size=step)
     dt = time.perf_counter() - t0
-    return nx * ny * nzs * res.iterations, dt
+    return nx * ny * nzs * res.iterations, dt, (res.x if want_x else None), list(res.history)
 
 
-def cpu_sample_spec(cfg, planes=16, iters=1):
+def cpu_kind():
+    return "reference" if reference_module() is not None else "port"
+
+
+def cpu_sample_spec(cfg, planes=REF_PLANES, iters=REF_ITERS):
     nx, ny, nz, _, _, _, l1, tv, inner, _ = cfg
-    return planes, iters, f"{nx}x{ny}x{planes} planes x {iters} FISTA iteration (step 1/(2*{planes})), " \
-                          f"same hologram, lambda=({l1},{tv}), T={inner}; per-voxel cost is nz-independent"
+    who = "holotrack.solver.fista (baseline/_ref)" if cpu_kind() == "reference" else "oracle port"
+    return planes, iters, f"{who}: {nx}x{ny}x{planes} planes x {iters} FISTA iterations from x=0 " \
+                          f"(initial step 1/(2*{planes})), the bench hologram, lambda=({l1},{tv}), T={inner}; " \
+                          f"per-voxel cost is nz-independent"
 
 
 def cpu_baseline(cfg, b):
+    """1-core CPU leg on rank 0; also returns the sample's volume/history for
+    the GPU-vs-CPU parity check."""
     planes, iters, desc = cpu_sample_spec(cfg)
     nx, ny, _, _, _, _, l1, tv, inner, _ = cfg
-    vox, dt = _cpu_sample((b, nx, ny, planes, iters, l1, tv, inner))
-    return {"value": vox / dt, "unit": "voxel-iter/s", "cores": 1, "kind": "port",
-            "sample": desc + f"; {dt:.1f} s on 1 core"}
+    vox, dt, x, hist = _cpu_sample((b, nx, ny, planes, iters, l1, tv, inner, True))
+    return {"value": vox / dt, "unit": "voxel-iter/s", "cores": 1, "kind": cpu_kind(),
+            "sample": desc + f"; {dt:.1f} s on 1 core"}, x, hist
+
+
+def sample_parity(cfg, b, x_cpu, hist_cpu, dev):
+    """The GPU path (public fista()) on the CPU leg's sample: same hologram,
+    geometry, step and iterations; volume rel-L2 and history agreement."""
+    from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, VolumeGeometry, fista
+    nx, ny, _, _, _, _, l1, tv, inner, _ = cfg
+    planes, iters, _ = cpu_sample_spec(cfg)
+    g = VolumeGeometry(nx, ny, planes, PITCH, DZ, Z0, LAM)
+    scfg = SolverConfig(weights=RegularizerWeights(l1, tv), max_iters=iters, tv_inner_iters=inner,
+                        step_size=1.0 / (2.0 * planes))
+    vol, rep = fista(ComplexField2D(b, PITCH, LAM), g, scfg)
+    x = vol.to_dense()
+    rel = float(np.linalg.norm(x - x_cpu) / max(np.linalg.norm(x_cpu), 1e-300))
+    hrel = float(max(abs(a - c) / max(abs(c), 1e-300) for a, c in zip(rep.objective, hist_cpu))) \
+        if len(hist_cpu) else 0.0
+    return {"rel_l2": rel, "history_max_rel": hrel, "iterations_equal": rep.iterations == len(hist_cpu),
+            "against": cpu_kind(), "bar": "rel_l2 <= 1e-4 (north_star)"}
 
 
 def run_reference(a, cfg_name):
-    """--impl reference: the CPU oracle port (the reference is pure Python and
-    cannot travel to the box) on every host core, one independent solve per
-    core (like holotrack's `reconstruct --workers`)."""
+    """--impl reference: the reference's own CPU implementation on every host
+    core, one independent solve per core per step (like holotrack's
+    `reconstruct --workers`), on the GPU arm's hologram."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import multiprocessing as mp
     cfg = CONFIGS[cfg_name]
     nx, ny, nz, iters_full, _, seed, l1, tv, inner, d = cfg
-    from oracle.holo_oracle import Geometry, add_noise, invert_residual, make_scene
-    # bounded CPU render of a sample hologram: 400 particles keep it ~40 s
-    g = Geometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
-    rng_pts = make_scene(min(400, n_particles(cfg)), g, d, seed=seed, margin_planes=2)
-    from oracle.holo_oracle import render_hologram
-    b = invert_residual(add_noise(render_hologram(rng_pts, g, d), 0.02, seed=seed + 7))
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     planes, iters, desc = cpu_sample_spec(cfg)
-    job = (b, nx, ny, planes, iters, l1, tv, inner)
+    # workers are forked before this process touches CUDA (GPU input render below)
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
+        b = reference_hologram(cfg)
+        job = (b, nx, ny, planes, iters, l1, tv, inner, False)
         for _ in range(a.warmup):
             pool.map(_cpu_sample, [job] * cores)
         times = []
@@ -210,10 +270,44 @@ def run_reference(a, cfg_name):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg_name}: {nx}x{ny}x{nz}, {iters_full} iterations (sampled)",
                        "sample": desc}, "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "voxel-iter/s", "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": "voxel-iter/s", "cores": cores, "kind": cpu_kind(),
                              "sample": desc + f"; {cores} concurrent solves (one per core)"},
             "e2e": {"value": value, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def reference_hologram(cfg):
+    """The GPU arm's hologram (make_hologram: same scene, render, noise); on a
+    host without a GPU only the small C1 scene can be rendered, by the oracle."""
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except ImportError:
+        gpu = False
+    if gpu:
+        return make_hologram(cfg)
+    if cfg is not CONFIGS["c1"]:
+        raise SystemExit("the reference arm needs a GPU to render this config's hologram")
+    from oracle.holo_oracle import Geometry, add_noise, invert_residual, make_scene, render_hologram
+    nx, ny, nz, _, _, seed, _, _, _, d = cfg
+    g = Geometry(nx, ny, nz, PITCH, DZ, Z0, LAM)
+    pts = make_scene(n_particles(cfg), g, d, seed=seed, margin_planes=2)
+    return invert_residual(add_noise(render_hologram(pts, g, d), 0.02, seed=seed + 7))
+
+
+def self_launch(a):
+    """`bench.py --gpus N` without torchrun: relaunch under torchrun, one rank
+    per GPU (NCCL_DEBUG=INFO so the communicator lines show the N ranks)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # ------------------------------------------------------------- GPU arm -----
@@ -229,6 +323,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     if a.impl == "reference":
         run_reference(a, a.config)
         return
@@ -238,6 +334,8 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -391,9 +489,10 @@ def main():
         e2e = {"value": e_vox / e_s, "unit": "voxel-iter/s", "h2d_bytes_per_step": 8 * nx * ny,
                "d2h_bytes_per_step": 24 * nnz + 8 * nz + 8 * iters, "steps": e2e_steps}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, b)
+        cpu, x_cpu, hist_cpu = cpu_baseline(cfg, b)
+        parity = sample_parity(cfg, b, x_cpu, hist_cpu, dev)
 
     if rank == 0:
         line = {
@@ -426,6 +525,7 @@ def main():
             "solve": {"iterations": rep.iterations, "restarts": rep.restarts, "nnz": rep.nnz,
                       "final_sparsity": rep.final_sparsity, "attempts": rep.attempts},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
         }
         print(json.dumps(line), flush=True)

@@ -292,6 +292,9 @@ struct Engine {
   unsigned* pr_counter = nullptr;  // [2] threadfence-reduction counters
   int* pr_err = nullptr;
   unsigned long long pr_epoch = 0;
+  // a peer timeout leaves the ranks' epochs out of step: the handle is then
+  // unusable (every later call fails with this message) until recreated
+  bool peer_broken = false;
   std::vector<void*> pr_mapped;  // IPC mappings of the other ranks' buffers
   int ensure_peer_buffers() {
     if (pr_inbox) return HOLO_OK;
@@ -419,6 +422,9 @@ struct Engine {
       return fail(HOLO_ERR_UNSUPPORTED, "plane shape " + std::to_string(g.ny) + "x" + std::to_string(g.nx) +
                                             " unsupported: the B200 FFT handles powers of two in [8, 4096]");
     if (n < 1 || r < 0 || r >= n) return fail(HOLO_ERR_INVALID, "bad rank/nranks");
+    // every rank owns >= 1 plane: an empty shard would launch zero-sized grids
+    if (n > g.nz) return fail(HOLO_ERR_INVALID, "more ranks (" + std::to_string(n) + ") than planes (" +
+                                                     std::to_string(g.nz) + ")");
     kb = (int)((long long)g.nz * r / n);
     ke = (int)((long long)g.nz * (r + 1) / n);
     nzl = ke - kb;
@@ -579,7 +585,10 @@ struct Engine {
     int perr = 0;
     if (peer_on) HOLO_CUDA(cudaMemcpyAsync(&perr, pr_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     HOLO_CUDA(cudaStreamSynchronize(s));
-    if (perr) return fail(HOLO_ERR_NCCL, "peer spectrum reduction: a rank did not arrive (timeout)");
+    if (perr) {
+      peer_broken = true;
+      return fail(HOLO_ERR_NCCL, "peer spectrum reduction: a rank did not arrive (timeout)");
+    }
     HOLO_CUDA(prof.harvest());
     return HOLO_OK;
   }
@@ -611,6 +620,7 @@ struct Engine {
 
   // solver.py:225-247: power iteration of A^H A from v0 (unit norm)
   int power_iteration(const float2* v0, int iters, bool real, double& out, cudaStream_t s) {
+    if (peer_broken) return fail(HOLO_ERR_NCCL, "an earlier peer spectrum reduction timed out: recreate the handle");
     int rc = ensure_volume();
     if (rc) return rc;
     const long long n = (long long)nzl * P;
@@ -622,6 +632,11 @@ struct Engine {
     const int nb = vol_norm2_blocks(std::max(n, 1LL));
     double* part = nullptr;
     HOLO_CUDA(cudaMallocAsync(&part, sizeof(double) * nb, s));
+    struct FreeOnExit {  // every return path, early errors included
+      double*& p;
+      cudaStream_t st;
+      ~FreeOnExit() { if (p) cudaFreeAsync(p, st); }
+    } free_part{part, s};
     double nrm = 1.0;
     for (int it = 0; it < iters; ++it) {
       if ((rc = forward_spectrum(v, S[0], s))) return rc;  // v may be scratch: consumed in place
@@ -640,7 +655,6 @@ struct Engine {
       HOLO_CUDA(vol_rescale(scratch, n, scal, real ? 1 : 0, s));
       v = scratch;
     }
-    cudaFreeAsync(part, s);
     HOLO_CUDA(cudaStreamSynchronize(s));
     out = nrm;
     return HOLO_OK;
@@ -783,6 +797,9 @@ struct Engine {
     if (cfg.stop_tol < 0) return fail(HOLO_ERR_INVALID, "stop_tol must be nonnegative");
     if (cfg.step_policy != HOLO_POLICY_BACKTRACKING && cfg.step_policy != HOLO_POLICY_FIXED)
       return fail(HOLO_ERR_INVALID, "unknown step_policy");
+    if (peer_broken)
+      return fail(HOLO_ERR_NCCL, "an earlier peer spectrum reduction timed out: the rank group is out of step, "
+                                 "recreate the handle");
     if ((rc = load_b(b_dev, s))) return rc;
     last = holo_report{};
     history.clear();
