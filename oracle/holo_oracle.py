@@ -193,9 +193,10 @@ def _tv_cost(x, v, tau):
     return tau * tv_norm(x) + 0.5 * float(d @ d)
 
 
-def fgp_tv(v, tau: float, iters: int = 5):
+def fgp_tv(v, tau: float, iters: int = 5, guard: bool = True):
     """Beck-Teboulle fast gradient projection for the 2D TV prox, with the
-    per-plane 'never worse than v' guard (prox.py:104-148)."""
+    per-plane 'never worse than v' guard (prox.py:104-148).  guard=False
+    (tests only) returns the FGP output without the guard's select."""
     if tau < 0 or iters < 1:
         raise ValueError("bad tau / iters")
     v = np.asarray(v, dtype=np.float64)
@@ -219,6 +220,8 @@ def fgp_tv(v, tau: float, iters: int = 5):
         ex = nx_ + mom * (nx_ - px)
         py, px, t = ny_, nx_, t_next
     out = v - tau * _grad2_adj(py, px)
+    if not guard:
+        return out
     flat_o = out.reshape(-1, *out.shape[-2:])
     flat_v = v.reshape(-1, *v.shape[-2:])
     for i in range(flat_o.shape[0]):
@@ -237,14 +240,14 @@ def fgp_beta_schedule(iters: int):
     return out
 
 
-def fused_prox(v, tau_l1: float, tau_tv: float, iters: int = 5):
+def fused_prox(v, tau_l1: float, tau_tv: float, iters: int = 5, guard: bool = True):
     """prox_l1(prox_tv(Re) + i prox_tv(Im)) (prox.py:151-165, solver.py:139-144)."""
     v = np.asarray(v)
     if tau_tv > 0:
         if np.iscomplexobj(v):
-            w = fgp_tv(v.real, tau_tv, iters) + 1j * fgp_tv(v.imag, tau_tv, iters)
+            w = fgp_tv(v.real, tau_tv, iters, guard) + 1j * fgp_tv(v.imag, tau_tv, iters, guard)
         else:
-            w = fgp_tv(v, tau_tv, iters)
+            w = fgp_tv(v, tau_tv, iters, guard)
     else:
         w = v
     return soft_threshold(w, tau_l1)

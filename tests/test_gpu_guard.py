@@ -76,13 +76,14 @@ def test_strip_prox_guard_fixup_vs_oracle(T):
     ref = O.fused_prox(v, tau_l1, tau_tv, T)
     out = P.prox_fl(v, tau_l1, tau_tv, T)
     assert rel_l2(out, ref) <= 1e-5, rel_l2(out, ref)
+    # without the guard's select the fired planes would differ by percents
+    unguarded = O.fused_prox(v, tau_l1, tau_tv, T, guard=False)
     for k in range(3):
         assert rel_l2(out[k], ref[k]) <= 1e-5
-        # the fired part is exactly the soft-thresholded input
-        st = O.soft_threshold(v[k], tau_l1)
-        for j, part in enumerate((np.real, np.imag)):
-            if fired[k, j]:
-                assert np.max(np.abs(part(out[k]) - part(st))) < 1e-6
+        if fired[k].any():
+            assert rel_l2(out[k], unguarded[k]) > 1e-3
+        else:
+            assert rel_l2(out[k], unguarded[k]) <= 1e-5
 
 
 def _guard_geometry(n, nz):
