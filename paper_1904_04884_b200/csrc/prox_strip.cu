@@ -222,26 +222,6 @@ HD void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
   } while (!done);
 }
-HD void tma_region(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t* bar, const Work& wk) {
-  const int c0 = 2 * wk.tg.rj0, c1 = wk.plane * a.ny + wk.tg.ri0;
-  const bool use[kSlotArrays] = {true, a.beta != 0.f, a.grad != nullptr};
-  unsigned bytes = 0;
-#pragma unroll
-  for (int k = 0; k < kSlotArrays; ++k) bytes += use[k] ? kArrayBytes : 0u;
-  // the slot was last read through the generic proxy (behind a CTA barrier)
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-#pragma unroll
-  for (int k = 0; k < kSlotArrays; ++k) {
-    if (!use[k]) continue;
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-            smem_u32(slot + k * kSlotF4)),
-        "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-  }
-}
-
 // strip walk: x and grad into buffer `buf`; the barrier expects x_prev's bytes
 // too (tma_xprev, issued later, completes it)
 HD void tma_box(const TmaMaps& maps, int k, float4* dst, uint64_t* bar, int c0, int c1) {
@@ -330,12 +310,21 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   }
   const bool cInt = gj >= j0 && gj < j1;
   const long long g0 = wk.g0;
+  constexpr bool staged = PH <= 1;
+  // Staged kernels keep x and grad double-buffered ([buf][x, grad]) and x_prev
+  // in one slot after them, refilled for the next region once every thread
+  // has read it (after iteration 0's barrier; without TV after the x_new one).
+  constexpr bool SPLITXP = staged;
+  // single pass with TV: the epilogue's w = v - tau D^T p takes the band
+  // below's non-extrapolated row-0 p from ptop (published with every FGP
+  // step), and w / x_new cross bands in one CTA barrier (top[0] / top[1])
+  constexpr bool FUSED_EPI = TV && PH == 0;
+  float4* ptop = save;  // [NW + 1][32] (single pass: the walk's save area)
   // this thread's float4 (2 columns) of row s of array k in the staged slot
   auto slot = [&](int k, int s) {
-    if constexpr (WALK) return (k == 1 ? stage + kXpSlot : pre + (k ? kSlotF4 : 0))[(r0 + s) * (RW / 2) + lane];
+    if constexpr (SPLITXP) return (k == 1 ? stage + kXpSlot : pre + (k ? kSlotF4 : 0))[(r0 + s) * (RW / 2) + lane];
     return pre[k * kSlotF4 + (r0 + s) * (RW / 2) + lane];
   };
-  constexpr bool staged = PH <= 1;
   // Strip walk: band 0 reads the rows above the frame, saved by the previous
   // region (rd), through bot[.][0], which it alone reads: it copies each saved
   // row in just before it is needed.  Band `saver` saves its last row into wr
@@ -493,8 +482,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     sm.bot[0][w + 1][lane] = f4(v[SR - 1][0], v[SR - 1][1]);
     save_rows(0, v);
     __syncthreads();
-    if constexpr (WALK) {  // every thread has read this region's x_prev: stream the next region's in
-      if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
+    if constexpr (SPLITXP) {  // every thread has read this region's x_prev: stream the next region's in
+      if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load<WALK>(a, *nxgeo));
     }
     {
       float2 up0 = above_of(0, 0, v[0][0]), up1 = above_of(0, 1, v[0][1]);
@@ -534,6 +523,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       xlast(xl0, xl1);
       sm.top[lastbuf][w][lane] = f4(rp[0][0], rp[0][1]);
       sm.bot[lastbuf][w + 1][lane] = f4(xl0, xl1);
+      if constexpr (FUSED_EPI) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
       save_x(1);
       band_arrive(&bbar[lastbuf]);
       fetch_above(lastbuf, 1);  // read by band 0 itself only: after its arrival
@@ -594,6 +584,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       xlast(xl0, xl1);
       sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
       sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
+      // (read only after the final band barrier; rewritten by the next region behind its iteration-0 barrier)
+      if constexpr (FUSED_EPI) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
       save_x(2 + t - tstart);
       band_arrive(&bbar[b ^ 1]);
       fetch_above(b ^ 1, 2 + t - tstart);
@@ -632,6 +624,52 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       }
       return;  // every band read of this region precedes the last sweep's barrier
     }
+    if constexpr (FUSED_EPI) {
+      // ---- w = v - tau D^T(p, q) (into rp), x_new = soft(w) (into p) ----
+      {
+        const float4 d4 = (!EDGE || w < NW - 1) ? ptop[(w + 1) * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int s = 0; s < SR; ++s) {
+          const float2 pd0 = (s < SR - 1) ? p[s + 1][0] : lo2(d4);
+          const float2 pd1 = (s < SR - 1) ? p[s + 1][1] : hi2(d4);
+          const float2 qr1 = right_of(q[s][0]);
+          rp[s][0] = fma2(mtau, sub2(sub2(add2(p[s][0], q[s][0]), pd0), q[s][1]), v[s][0]);
+          rp[s][1] = fma2(mtau, sub2(sub2(add2(p[s][1], q[s][1]), pd1), qr1), v[s][1]);
+        }
+      }
+      soft_rows();
+      // Last rows of w and x_new for the band below, in top[0] / top[1]: every
+      // band's reads of the band slots ended before its final-sweep arrival,
+      // and the next region writes top[] only behind its iteration-0 barrier
+      // (its pre-barrier write goes to bot[0]).
+      sm.top[0][w + 1][lane] = f4(rp[SR - 1][0], rp[SR - 1][1]);
+      sm.top[1][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+      __syncthreads();
+      // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
+      {
+        float2 up0 = rp[0][0], up1 = rp[0][1];
+        if (!top_rule()) {
+          const float4 b4 = sm.top[0][w][lane];
+          up0 = lo2(b4);
+          up1 = hi2(b4);
+        }
+#pragma unroll
+        for (int s = 0; s < SR; ++s) {
+          float2 gx0, gx1;
+          gx_row(rp[s][0], rp[s][1], gx0, gx1);
+          const float2 gy0 = sub2(rp[s][0], up0), gy1 = sub2(rp[s][1], up1);
+          up0 = rp[s][0];
+          up1 = rp[s][1];
+          if (rInt & (1u << s)) {
+            const float2 nw = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
+            const float2 d0 = sub2(rp[s][0], v[s][0]), d1 = sub2(rp[s][1], v[s][1]);
+            const float2 dd = fma2(d0, d0, mul2(d1, d1));
+            acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f, dd.x, acc[PT_G_R]));
+            acc[PT_G_I] = fmaf(ttv, nw.y, fmaf(0.5f, dd.y, acc[PT_G_I]));
+          }
+        }
+      }
+    } else {
     // ---- w = v - tau D^T(p, q) with the non-extrapolated dual (into rp) ----
     const int bf = lastbuf ^ 1;  // read by the last sweep, which every band has finished
     sm.top[bf][w][lane] = f4(p[0][0], p[0][1]);
@@ -671,6 +709,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         }
       }
     }
+    }  // !FUSED_EPI
   } else {
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
@@ -684,15 +723,29 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   // goes to bot[0] and its first-sweep publication follows a CTA barrier)
   constexpr int xb = TV ? 1 : 0;
 
-  sm.bot[xb][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
-  save_rows(kSaveX, p);
-  fetch_above(xb, kSaveX);
-  __syncthreads();
-  if constexpr (WALK && !TV) {  // (TV: issued after iteration 0's barrier)
-    if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load(a, *nxgeo));
+  if constexpr (!FUSED_EPI) {
+    sm.bot[xb][w + 1][lane] = f4(p[SR - 1][0], p[SR - 1][1]);
+    save_rows(kSaveX, p);
+    fetch_above(xb, kSaveX);
+    __syncthreads();
+  }
+  if constexpr (SPLITXP && !TV) {  // (TV: issued after iteration 0's barrier)
+    if (threadIdx.x == 0 && next_work >= 0) tma_xprev(a, maps, stage, nbar, geo_load<WALK>(a, *nxgeo));
   }
   {
-    float2 up0 = above_of(xb, 0, p[0][0]), up1 = above_of(xb, 1, p[0][1]);
+    float2 up0, up1;
+    if constexpr (FUSED_EPI) {
+      up0 = p[0][0];
+      up1 = p[0][1];
+      if (!top_rule()) {
+        const float4 b4 = sm.top[1][w][lane];
+        up0 = lo2(b4);
+        up1 = hi2(b4);
+      }
+    } else {
+      up0 = above_of(xb, 0, p[0][0]);
+      up1 = above_of(xb, 1, p[0][1]);
+    }
     const float2 cb = splat2(1.f + a.beta), cm = splat2(-a.beta);
 #pragma unroll
     for (int s = 0; s < SR; ++s) {
@@ -712,7 +765,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         float2 y[2] = {lo2(y4), hi2(y4)};
         if (a.beta != 0.f) {
           // (strip walk: x_prev's slot may already hold the next region's)
-          const float4 o = (staged && !WALK) ? slot(1, s) : *reinterpret_cast<const float4*>(a.xp + g);
+          const float4 o = *reinterpret_cast<const float4*>(a.xp + g);
           y[0] = fma2(cb, y[0], mul2(cm, lo2(o)));
           y[1] = fma2(cb, y[1], mul2(cm, hi2(o)));
         }
@@ -821,12 +874,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   }
   __syncthreads();
   if (leader) {
-    const Work w0 = geo_load(a, geo[0]);
-    if (WALK && staged) {
+    const Work w0 = geo_load<WALK>(a, geo[0]);
+    if (staged) {  // [buf][x, grad] + one x_prev slot
       tma_region_walk(a, maps, pre, &bars[0], w0);
       tma_xprev(a, maps, pre, &bars[0], w0);
-    } else if (staged) {
-      tma_region(a, maps, pre, &bars[0], w0);
     } else {
       tma_state(a, maps, pre, &bars[0], w0);
     }
@@ -839,15 +890,12 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     if (leader && nw >= 0) {
       const Work wn = work_geom<WALK>(a, nw);
       geo_store(geo[buf ^ 1], wn);
-      if (WALK && staged)
-        tma_region_walk(a, maps, pre + (buf ^ 1) * 2 * kSlotF4, &bars[buf ^ 1], wn);
-      else if (staged)
-        tma_region(a, maps, pre + (buf ^ 1) * kSlotArrays * kSlotF4, &bars[buf ^ 1], wn);
+      if (staged) tma_region_walk(a, maps, pre + (buf ^ 1) * 2 * kSlotF4, &bars[buf ^ 1], wn);
     }
     const Work cur = geo_load<WALK>(a, geo[buf]);
     // x / x_prev / grad slots double-buffered (first pass); one state slot (later passes)
     const int sb = staged ? buf : 0;
-    float4* slot = pre + sb * (WALK ? 2 : kSlotArrays) * kSlotF4;
+    float4* slot = pre + sb * 2 * kSlotF4;  // (later passes: the state slot at pre)
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
     if (cur.edge)
@@ -946,8 +994,8 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   static_assert(kStateBytes == sizeof(float4) * kStageWalkF4, "later passes' state slot = the walk stage area");
-  const size_t smem = a.walk ? sizeof(Bands) + sizeof(float4) * (kStageWalkF4 + 2 * kSaveSlots * 32)
-                             : sizeof(Bands) + sizeof(float4) * 2 * kSlotArrays * kSlotF4;
+  // [2][x, grad] + x_prev (+ the walk's saved rows / the single pass's ptop)
+  const size_t smem = sizeof(Bands) + sizeof(float4) * (kStageWalkF4 + (a.walk ? 2 * kSaveSlots * 32 : (NW + 1) * 32));
   TmaMaps maps;
   memset(&maps, 0, sizeof(maps));
   const int rows = a.nplanes * a.ny;
