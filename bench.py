@@ -323,7 +323,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     a = ap.parse_args()
-    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    # (HOLO_SELF_LAUNCH=1: also for one GPU, e.g. with HOLO_NCCL_SINGLE_RANK=1 to run the
+    # torchrun + NCCL plumbing of the sharded engine on a single-GPU box)
+    if (a.gpus > 1 or os.environ.get("HOLO_SELF_LAUNCH") == "1") and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(a))
     if a.impl == "reference":
         run_reference(a, a.config)
