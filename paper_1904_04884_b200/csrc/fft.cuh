@@ -22,6 +22,8 @@
 // pi i m/N) (fp64-exact entries rounded to fp32) held in shared memory, so a
 // table twiddle multiply is one FMUL2 + one FFMA2.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace holo {
@@ -270,6 +272,39 @@ struct Dft<64, INV> {
     combine<0>(ev, od, a);
   }
 };
+template <bool INV, int E, int R, int S, int RR>
+HD void rot_apply(float2 (&a)[R]);
+// x * exp(-/+ 2 pi i e / E), e compile-time, E in {8, 16, 32, 64}
+template <bool INV, int E, int e>
+HD float2 rotE(float2 x) {
+  if constexpr (E == 64)
+    return rot64<INV, e>(x);
+  else
+    return rot32<INV, e * (32 / E)>(x);
+}
+template <bool INV, int E, int R, int S, int RR>
+HD void rot_apply(float2 (&a)[R]) {
+  if constexpr (RR < R) {
+    a[RR] = rotE<INV, E, (S * RR) % E>(a[RR]);
+    rot_apply<INV, E, R, S, RR + 1>(a);
+  }
+}
+// last-pass twiddles of butterfly s: table twiddle of butterfly 0 (t0[r-1]),
+// then the compile-time rotation by s r / E turns (S runs over 0..E-1 so s
+// can be matched against a template argument)
+template <bool INV, int E, int R, int S>
+HD void rot_twiddles(float2 (&a)[R], const float4 (&t0)[R - 1], std::integral_constant<int, S>, int s) {
+  if constexpr (S < E / R) {
+    if (s == S) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) a[r] = twiddle<INV>(a[r], t0[r - 1]);
+      rot_apply<INV, E, R, S, 1>(a);
+    } else {
+      rot_twiddles<INV, E, R, S + 1>(a, t0, std::integral_constant<int, S + 1>(), s);
+    }
+  }
+}
+
 // One Stockham pass of radix R with NS = product of earlier radices.
 template <int N, int E, int R, int NS, bool INV, bool FIRST, bool LAST>
 HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __restrict__ tw) {
@@ -290,13 +325,49 @@ HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __rest
   } else if constexpr (!LAST) {
     __syncthreads();  // buffer may still be read by a previous transform's last pass
   }
+  // Twiddle loads are shared-memory wavefronts, the bound of the column
+  // passes (a quarter of their wavefronts at N = 1024, E = 16), so:
+  // * the last pass with several butterflies per thread (BPT > 1) loads the
+  //   s = 0 butterfly's R-1 twiddles once: butterfly s has kk = j + s TPF < NS
+  //   and w^(kk r) = w^(j r) exp(-/+ 2 pi i s r / E), a compile-time rotation;
+  // * a radix-16 pass factors w^(kk r) = w^(kk r1) w^(kk 4 r2), r = r1 + 4 r2:
+  //   6 table loads instead of 15 (one more rounding where both are nonzero).
+  constexpr bool kRotLast = LAST && BPT > 1 && NS > 1;
+  constexpr bool kSplit16 = !kRotLast && R == 16 && NS > 1;
+  float4 t0[kRotLast ? R - 1 : 1];
+  if constexpr (kRotLast) {
+    const float4* tp = tw + TwLayout<N, E>::offset(NS) + j;  // kk of butterfly s = 0
+#pragma unroll
+    for (int r = 1; r < R; ++r) t0[r - 1] = tp[(r - 1) * NS];
+  }
 #pragma unroll
   for (int s = 0; s < BPT; ++s) {
     const int b = j + s * TPF;
     float2 a[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = v[s + r * BPT];
-    if constexpr (NS > 1) {
+    if constexpr (kRotLast) {
+      rot_twiddles<INV, E, R>(a, t0, std::integral_constant<int, 0>(), s);
+    } else if constexpr (kSplit16) {
+      const int kk = b % NS;
+      const float4* tp = tw + TwLayout<N, E>::offset(NS) + kk;
+      {  // w^(kk 4 r2), r2 = 1..3, on a[4 r2 .. 4 r2 + 3]
+        float4 th[3];
+#pragma unroll
+        for (int r2 = 1; r2 < 4; ++r2) th[r2 - 1] = tp[(4 * r2 - 1) * NS];
+#pragma unroll
+        for (int r = 4; r < 16; ++r) a[r] = twiddle<INV>(a[r], th[r / 4 - 1]);
+      }
+      asm volatile("" ::: "memory");
+      {  // w^(kk r1), r1 = 1..3, on a[r1 + 4 r2]
+        float4 tl[3];
+#pragma unroll
+        for (int r1 = 1; r1 < 4; ++r1) tl[r1 - 1] = tp[(r1 - 1) * NS];
+#pragma unroll
+        for (int r = 1; r < 16; ++r)
+          if (r % 4) a[r] = twiddle<INV>(a[r], tl[r % 4 - 1]);
+      }
+    } else if constexpr (NS > 1) {
       const int kk = b % NS;
       const float4* tp = tw + TwLayout<N, E>::offset(NS) + kk;
       // groups of 4 twiddles: bounds the 4-register table entries in flight
