@@ -129,14 +129,17 @@ class ClockSampler:
 
 def measured_traffic(kernel, voxels):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, scaled from
-    the committed ncu --set full capture of one launch (profiles/r01_traffic.json,
-    written by tools/ncu_traffic.py); None if that kernel was not captured."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            rec = json.load(f).get(kernel)
-    except (OSError, ValueError):
-        return None
-    return None if rec is None else rec["dram_bytes_per_voxel"] * voxels
+    the committed ncu --set full capture of one launch (profiles/r02_traffic.json,
+    else r01; written by tools/ncu_traffic.py); None if that kernel was not captured."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):  # latest capture first
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                rec = json.load(f).get(kernel)
+        except (OSError, ValueError):
+            continue
+        if rec is not None:
+            return rec["dram_bytes_per_voxel"] * voxels
+    return None
 
 
 def peaks():
