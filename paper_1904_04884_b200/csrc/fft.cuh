@@ -45,25 +45,42 @@ struct FftShape {
   static constexpr int PADN = N + N / E + (TPF >= 16 ? 2 : TPF);
 };
 
-// Twiddle tables are stored per pass as [r-1][kk] (kk = butterfly index mod
+// Twiddle tables are stored per pass as [row][kk] (kk = butterfly index mod
 // NS), so the lanes of a warp (consecutive kk) read consecutive entries:
 // conflict-free, or broadcast.  Entry = (w, conj w), w = exp(-2 pi i kk r/(NS R)).
+// Only the twiddles fft_pass loads are stored (compact, so the row kernel's
+// shared copy is small):
+// * the last pass with several butterflies per thread (rotlast): rows
+//   r = 1..R-1, kk < TPF only (the other butterflies rotate these);
+// * radix-16 / -32 passes (split): rows r = 1, 2, 3 then r = 4, 8, ..., R-4;
+// * other passes: rows r = 1..R-1.
 template <int N, int E = DefaultE<N>::value>
 struct TwLayout {
   static constexpr int radix(int ns) { return ((N / ns) % E == 0) ? E : N / ns; }
+  static constexpr bool rotlast(int ns) { return ns * radix(ns) == N && E / radix(ns) > 1; }
+  static constexpr bool split(int ns) { return !rotlast(ns) && (radix(ns) == 16 || radix(ns) == 32); }
+  static constexpr int rows(int ns) { return split(ns) ? radix(ns) / 4 + 2 : radix(ns) - 1; }
+  static constexpr int cols(int ns) { return rotlast(ns) ? N / E : ns; }
+  // table row of twiddle power r (split passes)
+  static constexpr int row_of(int ns, int r) { return split(ns) ? (r < 4 ? r - 1 : 2 + r / 4) : r - 1; }
   // offset of the table of the pass whose product of earlier radices is ns
   static constexpr int offset(int ns) {
     int off = 0;
-    for (int s = E; s < ns; s *= radix(s)) off += (radix(s) - 1) * s;
+    for (int s = E; s < ns; s *= radix(s)) off += rows(s) * cols(s);
     return off;
   }
   static constexpr int size() {
     if (N <= E) return 1;
     int off = 0;
-    for (int s = E; s < N; s *= radix(s)) off += (radix(s) - 1) * s;
+    for (int s = E; s < N; s *= radix(s)) off += rows(s) * cols(s);
     return off;
   }
 };
+// float2 slots of a kernel's shared copy of the table (128-byte multiple)
+template <int N, int E>
+constexpr int tw_f2() {
+  return (2 * TwLayout<N, E>::size() + 15) & ~15;
+}
 
 template <int SH>
 HD int fft_pad(int i) { return i + (i >> SH); }
@@ -335,13 +352,15 @@ HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __rest
   //   where both factors are nonzero.  Measured (C3, 10 iterations): adjoint
   //   columns 12.18 -> 11.16 ms, forward columns 12.34 -> 12.08, row passes
   //   15.22 / 14.97 -> 14.49 / 14.24.
-  constexpr bool kRotLast = LAST && BPT > 1 && NS > 1;
-  constexpr bool kSplit = !kRotLast && (R == 16 || R == 32) && NS > 1;
+  using TL = TwLayout<N, E>;
+  constexpr bool kRotLast = NS > 1 && TL::rotlast(NS);
+  constexpr bool kSplit = NS > 1 && TL::split(NS);
+  static_assert(!kRotLast || (LAST && BPT > 1), "");
   float4 t0[kRotLast ? R - 1 : 1];
   if constexpr (kRotLast) {
-    const float4* tp = tw + TwLayout<N, E>::offset(NS) + j;  // kk of butterfly s = 0
+    const float4* tp = tw + TL::offset(NS) + j;  // kk of butterfly s = 0
 #pragma unroll
-    for (int r = 1; r < R; ++r) t0[r - 1] = tp[(r - 1) * NS];
+    for (int r = 1; r < R; ++r) t0[r - 1] = tp[(r - 1) * TL::cols(NS)];
   }
 #pragma unroll
   for (int s = 0; s < BPT; ++s) {
@@ -353,11 +372,11 @@ HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __rest
       rot_twiddles<INV, E, R>(a, t0, std::integral_constant<int, 0>(), s);
     } else if constexpr (kSplit) {
       const int kk = b % NS;
-      const float4* tp = tw + TwLayout<N, E>::offset(NS) + kk;
+      const float4* tp = tw + TL::offset(NS) + kk;
       {  // w^(kk 4 r2), r2 = 1..R/4-1, on a[4 r2 .. 4 r2 + 3]
         float4 th[R / 4 - 1];
 #pragma unroll
-        for (int r2 = 1; r2 < R / 4; ++r2) th[r2 - 1] = tp[(4 * r2 - 1) * NS];
+        for (int r2 = 1; r2 < R / 4; ++r2) th[r2 - 1] = tp[TL::row_of(NS, 4 * r2) * NS];
 #pragma unroll
         for (int r = 4; r < R; ++r) a[r] = twiddle<INV>(a[r], th[r / 4 - 1]);
       }
@@ -365,14 +384,14 @@ HD void fft_pass(float2 (&v)[E], int j, float2* buf, int S, const float4* __rest
       {  // w^(kk r1), r1 = 1..3, on a[r1 + 4 r2]
         float4 tl[3];
 #pragma unroll
-        for (int r1 = 1; r1 < 4; ++r1) tl[r1 - 1] = tp[(r1 - 1) * NS];
+        for (int r1 = 1; r1 < 4; ++r1) tl[r1 - 1] = tp[TL::row_of(NS, r1) * NS];
 #pragma unroll
         for (int r = 1; r < R; ++r)
           if (r % 4) a[r] = twiddle<INV>(a[r], tl[r % 4 - 1]);
       }
     } else if constexpr (NS > 1) {
       const int kk = b % NS;
-      const float4* tp = tw + TwLayout<N, E>::offset(NS) + kk;
+      const float4* tp = tw + TL::offset(NS) + kk;
       // groups of 4 twiddles: bounds the 4-register table entries in flight
 #pragma unroll
       for (int r0 = 1; r0 < R; r0 += 4) {

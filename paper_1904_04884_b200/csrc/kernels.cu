@@ -74,18 +74,20 @@ constexpr int tw_slot() { return E >= 32 ? 1 : 0; }
 template <int N, int E>
 __global__ void k_twiddles(float4* tw) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= TwLayout<N, E>::size()) return;
+  using TL = TwLayout<N, E>;
+  if (e >= TL::size()) return;
   int off = 0;
-  for (int ns = E; ns < N; ns *= TwLayout<N, E>::radix(ns)) {
-    const int R = TwLayout<N, E>::radix(ns);
-    if (e < off + (R - 1) * ns) {
-      const int r = 1 + (e - off) / ns, kk = (e - off) % ns;
+  for (int ns = E; ns < N; ns *= TL::radix(ns)) {
+    const int R = TL::radix(ns), cols = TL::cols(ns), n = TL::rows(ns) * cols;
+    if (e < off + n) {
+      const int row = (e - off) / cols, kk = (e - off) % cols;
+      const int r = TL::split(ns) ? (row < 3 ? row + 1 : 4 * (row - 2)) : row + 1;
       double sn, cs;
       sincospi(-2.0 * (double)kk * r / ((double)ns * R), &sn, &cs);
       tw[e] = make_float4((float)cs, (float)sn, (float)cs, (float)-sn);
       return;
     }
-    off += (R - 1) * ns;
+    off += n;
   }
 }
 
@@ -129,6 +131,15 @@ __global__ void k_phase(uint64_t* tab, uint8_t* mask, int ny, int nx, double pit
 
 // ------------------------------------------------------------- K3 rows -----
 
+// Shared twiddle slots of the row kernel: the compact table for 2048-point
+// rows (C4 row passes 71.3 -> 65.6 ms per 5 iterations); 1024-point rows keep
+// the full-size slot, i.e. 4 CTAs per SM -- at 5 (compact table) the C3 row
+// passes slowed 14.45 -> 16.4 ms per 10 iterations.
+template <int N, int E>
+constexpr int row_tw_f2() {
+  return N >= 2048 ? tw_f2<N, E>() : 2 * N;
+}
+
 template <int N, bool INV, int E_>
 __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
                                                           long long nrows, float scale, const float4* __restrict__ twg) {
@@ -137,7 +148,7 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
   constexpr int RPC = row_threads<E_>() / TPF;
   extern __shared__ float2 smem[];
   float4* tw = reinterpret_cast<float4*>(smem);
-  float2* buf = smem + 2 * N;
+  float2* buf = smem + row_tw_f2<N, E_>();
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   __syncthreads();
   const int lr = threadIdx.x / TPF, j = threadIdx.x % TPF;
@@ -1021,7 +1032,7 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
     using Sh = FftShape<N, E>;
     constexpr int NT = row_threads<E>();
     constexpr int RPC = NT / Sh::TPF;
-    const size_t smem = sizeof(float2) * (2 * N + (size_t)RPC * Sh::PADN);
+    const size_t smem = sizeof(float2) * (row_tw_f2<N, E>() + (size_t)RPC * Sh::PADN);
     const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
     if (inverse) {
       err = set_smem(k_fft_rows<N, true, E>, smem);
