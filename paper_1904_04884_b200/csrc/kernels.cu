@@ -134,7 +134,8 @@ __global__ void k_phase(uint64_t* tab, uint8_t* mask, int ny, int nx, double pit
 // Shared twiddle slots of the row kernel: the compact table for 2048-point
 // rows (C4 row passes 71.3 -> 65.6 ms per 5 iterations); 1024-point rows keep
 // the full-size slot, i.e. 4 CTAs per SM -- at 5 (compact table) the C3 row
-// passes slowed 14.45 -> 16.4 ms per 10 iterations.
+// passes slowed 14.45 -> 16.4 ms per 10 iterations, at 3 they are unchanged,
+// at 2 they take 23.2 / 19.4.
 template <int N, int E>
 constexpr int row_tw_f2() {
   return N >= 2048 ? tw_f2<N, E>() : 2 * N;
