@@ -1,12 +1,14 @@
-"""End-to-end parity at the BENCHMARKED plane size (1024x1024, the C2/C3/C5
-lateral size) against the fp64 oracle (pinned to the reference by
-test_oracle.py): fista() on 1024^2 x 16 planes, the bench's own sampled
-configuration.
+"""End-to-end parity at the BENCHMARKED plane sizes (1024x1024, the C2/C3/C5
+lateral size, and 2048x2048, C4's) against the fp64 oracle (pinned to the
+reference by test_oracle.py): fista() on 1024^2 x 16 planes (the bench's
+own sampled configuration) and 2048^2 x 4 planes.
 
 * C3 weights: lambda = (0.5, 0.2), T = 5 -> the single-pass strip prox with
   many persistent regions per SM, interior and edge instantiations;
 * C5 weights: lambda = (0.05, 1.0), T = 20 -> the multi-pass strip walk
-  (7 + 7 + 6 FGP steps) with saved rows at production width.
+  (7 + 7 + 6 FGP steps) with saved rows at production width;
+* C4's plane size with C3's weights: 2048-point rows (radix-64 + 32) and
+  columns (16 x 16 x 8), 40 x 40 prox regions per plane.
 
 Bar (north_star): identical iterations / restarts / accepted step, history
 within 2e-5, volume rel-L2 <= 1e-4, identical detected-particle counts
@@ -23,26 +25,26 @@ from oracle import holo_oracle as O
 pytestmark = pytest.mark.gpu
 
 PITCH, DZ, Z0, LAM = 10e-6, 10e-6, 5e-3, 632e-9
-NX = NY = 1024
-NZ = 16
 CASES = {
-    # name: (particles, rods?, seed, lam_l1, lam_tv, T, iterations)
-    "c3": (1500, False, 2, 0.5, 0.2, 5, 5),
-    "c5": (120, True, 4, 0.05, 1.0, 20, 3),
+    # name: (n, nz, particles, rods?, seed, lam_l1, lam_tv, T, iterations)
+    "c3": (1024, 16, 1500, False, 2, 0.5, 0.2, 5, 5),
+    "c5": (1024, 16, 120, True, 4, 0.05, 1.0, 20, 3),
+    "c4": (2048, 4, 2000, False, 3, 0.5, 0.2, 5, 3),
 }
 
 
-def _geom():
+def _geom(name):
     from paper_1904_04884_b200 import VolumeGeometry
-    return VolumeGeometry(NX, NY, NZ, PITCH, DZ, Z0, LAM)
+    n, nz = CASES[name][:2]
+    return VolumeGeometry(n, n, nz, PITCH, DZ, Z0, LAM)
 
 
 def _hologram(name):
-    """Seeded scene inside the 16-plane volume, rendered on the GPU (input
+    """Seeded scene inside the case's volume, rendered on the GPU (input
     generation; both sides get the same b)."""
     from paper_1904_04884_b200.synth import add_noise, generate_scene, invert_residual, render_hologram
-    n, rods, seed, *_ = CASES[name]
-    sc = generate_scene(n, _geom(), 20e-6, seed=seed, margin_planes=2)
+    _, nz, n, rods, seed, *_ = CASES[name]
+    sc = generate_scene(n, _geom(name), 20e-6, seed=seed, margin_planes=1 if nz < 8 else 2)
     if rods:  # microfibres: random unit orientation, length 10 d (SURVEY 8d C5)
         rng = np.random.default_rng(seed + 100)
         for p in sc.particles:
@@ -53,10 +55,10 @@ def _hologram(name):
 
 def _oracle(args):
     b, name = args
-    _, _, _, l1, tv, T, iters = CASES[name]
-    g = O.Geometry(NX, NY, NZ, PITCH, DZ, Z0, LAM)
+    n, nz, _, _, _, l1, tv, T, iters = CASES[name]
+    g = O.Geometry(n, n, nz, PITCH, DZ, Z0, LAM)
     # the reference's power iteration returns nz to 1e-15
-    r = O.fista_solve(b, g, lam_l1=l1, lam_tv=tv, max_iters=iters, inner=T, step_size=1.0 / (2.0 * NZ))
+    r = O.fista_solve(b, g, lam_l1=l1, lam_tv=tv, max_iters=iters, inner=T, step_size=1.0 / (2.0 * nz))
     return r.x.astype(np.complex64), r.history, r.iterations, r.restarts, r.step
 
 
@@ -73,30 +75,32 @@ def solves():
 
 def _gpu(b, name):
     from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, fista
-    _, _, _, l1, tv, T, iters = CASES[name]
+    *_, l1, tv, T, iters = CASES[name]
     cfg = SolverConfig(weights=RegularizerWeights(l1, tv), max_iters=iters, tv_inner_iters=T)
-    vol, rep = fista(ComplexField2D(b, PITCH, LAM), _geom(), cfg)
+    vol, rep = fista(ComplexField2D(b, PITCH, LAM), _geom(name), cfg)
     for p in vol.planes:
         p.validate()
     return vol.to_dense(), rep
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_fista_1024_vs_oracle(solves, name):
+def test_fista_large_planes_vs_oracle(solves, name):
     _, gpu, ref = solves
     x, rep = gpu[name]
     rx, rhist, riters, rrest, rstep = ref[name]
     assert rep.iterations == riters and rep.restarts == rrest
     assert abs(rep.step_size - rstep) <= 1e-12 * rstep
     assert np.allclose(rep.objective, rhist, rtol=2e-5, atol=1e-9), (rep.objective, rhist)
+    print(f"{name}: rel-L2 {rel_l2(x, rx):.2e}, history max rel "
+          f"{np.max(np.abs(np.array(rep.objective) - rhist) / np.abs(rhist)):.2e}, nnz {np.count_nonzero(sx := x != 0)}")
     assert rel_l2(x, rx) <= 1e-4, rel_l2(x, rx)
     # support: nonzeros agree except at the soft-threshold boundary
-    sx, sr = x != 0, rx != 0
+    sr = rx != 0
     assert np.count_nonzero(sx ^ sr) <= 1e-4 * max(np.count_nonzero(sr), 1)
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_fista_1024_detections(solves, name):
+def test_fista_large_planes_detections(solves, name):
     _, gpu, ref = solves
     x, _ = gpu[name]
     rx = ref[name][0]
@@ -105,3 +109,4 @@ def test_fista_1024_detections(solves, name):
     assert d_ref.shape[0] > 0
     assert d_gpu.shape[0] == d_ref.shape[0]
     assert np.max(np.abs(d_gpu[:, :3] - d_ref[:, :3])) < 0.5
+    print(f"{name}: {d_ref.shape[0]} detections, max centroid diff {np.max(np.abs(d_gpu[:, :3] - d_ref[:, :3])):.2e} voxel")
