@@ -275,6 +275,20 @@ enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_
 struct Engine {
   holo_geometry geom{};
   int device = 0, rank = 0, nranks = 1, kb = 0, ke = 0, nzl = 0;
+  // Volume stack of the current solve.  Complex engine: nzs = nzl planes.
+  // Packed real engine (real_nonnegative): x is real, so stack plane k holds
+  // local real planes 2k (Re) and 2k+1 (Im), nzs = ceil(nzl / 2); the
+  // transfer weights become U_k = c_2k + i c_2k+1 (c = Re H, see k_adj_cols),
+  // the prox thresholds each part, and every volume kernel does half the
+  // work.  With odd nzl the last Im part is a dummy plane held at zero (its
+  // gradient is zeroed, so v, w and x_new stay 0 there).
+  int nzs = 0;
+  bool packed = false;
+  void set_stack(bool pk) {
+    packed = pk;
+    nzs = pk ? (nzl + 1) / 2 : nzl;
+  }
+  bool dummy_part() const { return packed && (nzl & 1); }
   long long P = 0;
   cudaStream_t stream = nullptr;
   Plan plan;
@@ -317,10 +331,10 @@ struct Engine {
   }
   // S_out = sum over ranks of sum over plane groups of Spart (replaces
   // sum_groups + the spectrum allreduce)
-  int peer_reduce(float2* S_out, cudaStream_t s) {
+  int peer_reduce(float2* S_out, int ngroups, cudaStream_t s) {
     const unsigned long long e = ++pr_epoch;
     const long long max_polls = 1LL << 26;  // ~20 s: a dead peer fails instead of hanging
-    HOLO_CUDA(peer_scatter(Spart, groups, P, pset, e, pr_counter, s));
+    HOLO_CUDA(peer_scatter(Spart, ngroups, P, pset, e, pr_counter, s));
     if (lgroup) HOLO_CUDA(lgroup->barrier(rank, s));  // one GPU: no kernel may wait on another rank's
     HOLO_CUDA(peer_wait(pset, 0, e, max_polls, pr_err, s));
     HOLO_CUDA(peer_gather(P, pset, e, pr_counter + 1, s));
@@ -428,6 +442,7 @@ struct Engine {
     kb = (int)((long long)g.nz * r / n);
     ke = (int)((long long)g.nz * (r + 1) / n);
     nzl = ke - kb;
+    set_stack(false);
     P = (long long)g.nx * g.ny;
     HOLO_CUDA(cudaSetDevice(dev));
     HOLO_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -549,22 +564,25 @@ struct Engine {
 
   // S_out = A x (spectrum, band mask not applied; allreduced over ranks)
   int forward_spectrum(const float2* x, float2* S_out, cudaStream_t s) {
-    PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzl * geom.ny, false, 1.0f, s));
-    PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzl, kb, groups, s));
+    const int g = std::min(groups, fwd_groups(plan, std::max(nzs, 1)));  // (Spart holds `groups` partials)
+    PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzs * geom.ny, false, 1.0f, s));
+    PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzs, kb, g, s, packed));
     if (peer_on && nranks > 1) {  // fused group sum + reduce-scatter + all-gather over peer memory
       HOLO_CUDA(prof.begin(PK_SUM_GROUPS, s));
-      int rc = peer_reduce(S_out, s);
+      int rc = peer_reduce(S_out, g, s);
       HOLO_CUDA(prof.end(s));
       return rc;
     }
-    PROF(PK_SUM_GROUPS, s, sum_groups(plan, Spart, groups, S_out, s));
+    PROF(PK_SUM_GROUPS, s, sum_groups(plan, Spart, g, S_out, s));
     return allreduce_spec(S_out, s);
   }
 
   // scratch = 2 A^H r with R the masked residual spectrum
   int adjoint_grad(const float2* Rm, float scale, cudaStream_t s) {
-    PROF(PK_ADJ_COLS, s, adj_cols(plan, Rm, scratch, nzl, kb, s));
-    PROF(PK_ADJ_ROWS, s, fft_rows(plan, scratch, scratch, (long long)nzl * geom.ny, true, scale / (float)P, s));
+    PROF(PK_ADJ_COLS, s, adj_cols(plan, Rm, scratch, nzs, kb, s, packed));
+    PROF(PK_ADJ_ROWS, s, fft_rows(plan, scratch, scratch, (long long)nzs * geom.ny, true, scale / (float)P, s));
+    // the dummy Im part of the last stack plane gets no gradient (stays 0)
+    if (dummy_part()) HOLO_CUDA(zero_imag(scratch + (size_t)(nzs - 1) * P, P, s));
     return HOLO_OK;
   }
 
@@ -603,7 +621,7 @@ struct Engine {
     PROF(PK_PROX, s, prox(a, s));
     HOLO_CUDA(prof.begin(PK_REDUCE, s));
     HOLO_CUDA(prox_reduce(a, a.tau_tv, a.tau_tv > 0.f, force_acc, plane_out, new_fail, s));
-    HOLO_CUDA(plane_total(plane_out, new_fail, nzl, scal, s));
+    HOLO_CUDA(plane_total(plane_out, new_fail, nzs, scal, s));
     HOLO_CUDA(prof.end(s));
     return allreduce_scalars(scal, SC_FAIL + 1, s);
   }
@@ -623,6 +641,7 @@ struct Engine {
     if (peer_broken) return fail(HOLO_ERR_NCCL, "an earlier peer spectrum reduction timed out: recreate the handle");
     int rc = ensure_volume();
     if (rc) return rc;
+    set_stack(false);  // the reference's start vector, one complex plane per real plane
     const long long n = (long long)nzl * P;
     counted_slot = -1;
     have_solution = false;
@@ -676,7 +695,7 @@ struct Engine {
     if (cfg.real_nonnegative && (rc = real_opnorm_value(sigma2, s))) return rc;
     for (;;) {
       ProxArgs a;
-      if ((rc = ensure_prox(a, nzl, geom.ny, geom.nx, cfg.tv_inner_iters, s))) return rc;
+      if ((rc = ensure_prox(a, nzs, geom.ny, geom.nx, cfg.tv_inner_iters, s))) return rc;
       // gradient 2 A^H r_y into scratch (the forward pass below reuses scratch,
       // so a backtracking retry recomputes it)
       if ((rc = adjoint_grad(R, 2.0f, s))) return rc;
@@ -692,7 +711,7 @@ struct Engine {
       a.real_mode = cfg.real_nonnegative ? 1 : 0;
       // ip / dx2 feed only the sufficient-decrease test, which is analytic below 1/(2 sigma^2)
       a.ipdx = (cfg.step_policy == HOLO_POLICY_BACKTRACKING && 2.0 * sigma2 * step > 1.0 + 1e-14) ? 1 : 0;
-      HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzl, 1), s));
+      HOLO_CUDA(cudaMemsetAsync(force_acc, 0, std::max(nzs, 1), s));
       if ((rc = prox_step(a, s))) return rc;
       // forward of the candidate (the adjoint scratch is consumed, reuse it)
       // and its data term, queued behind the prox without a host round trip:
@@ -748,6 +767,12 @@ struct Engine {
   int counted_slot = -1;  // slot whose chunk counts/offsets are current (host + device)
   long long counted_total = 0;
 
+  // the solution as one complex64 plane per local real plane: slot `slot`, or
+  // for the packed real engine its unpacked copy in scratch (made at the end
+  // of the solve; Im = 0)
+  bool sol_packed = false;  // the last solve ran the packed real engine
+  float2* sol_volume(int slot) { return sol_packed ? scratch : X[slot]; }
+
   int count_nnz(int slot, long long& total, std::vector<long long>* per_plane, cudaStream_t s) {
     const int nch = coo_chunks(P, std::max(nzl, 1));
     if (slot == counted_slot && nzl > 0) {  // the solution has not changed since the last count
@@ -768,7 +793,7 @@ struct Engine {
       if (per_plane) per_plane->clear();
       return HOLO_OK;
     }
-    HOLO_CUDA(coo_count(X[slot], P, nzl, coo_counts, s));
+    HOLO_CUDA(coo_count(sol_volume(slot), P, nzl, coo_counts, s));
     HOLO_CUDA(cudaMemcpyAsync(h_counts.data(), coo_counts, sizeof(int) * nch, cudaMemcpyDeviceToHost, s));
     HOLO_CUDA(cudaStreamSynchronize(s));
     const int cpp = nch / nzl;
@@ -801,6 +826,7 @@ struct Engine {
       return fail(HOLO_ERR_NCCL, "an earlier peer spectrum reduction timed out: the rank group is out of step, "
                                  "recreate the handle");
     if ((rc = load_b(b_dev, s))) return rc;
+    set_stack(cfg.real_nonnegative != 0);
     last = holo_report{};
     history.clear();
     have_solution = false;
@@ -866,6 +892,8 @@ struct Engine {
     }
     ix = sx;
     have_solution = true;
+    sol_packed = packed;
+    if (packed && nzl > 0) HOLO_CUDA(unpack_real(X[sx], scratch, nzl, P, s));
     long long nnz = 0;
     if ((rc = count_nnz(sx, nnz, nullptr, s))) return rc;
     if (nranks > 1) {
@@ -1212,7 +1240,8 @@ static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, void* vals, 
   if (tot > cap) return fail(HOLO_ERR_INVALID, "COO capacity too small");
   if (tot == 0) return HOLO_OK;
   if (!host) {
-    HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, rows, cols, (float2*)vals, nullptr, s));
+    HOLO_CUDA(holo::coo_compact(e.sol_volume(e.ix), e.P, e.geom.nx, e.nzl, e.coo_offsets, rows, cols, (float2*)vals,
+                                nullptr, s));
     return HOLO_OK;
   }
   if (tot > e.coo_cap) {  // grow-only device staging, reused across exports
@@ -1228,7 +1257,7 @@ static int export_coo(holo_handle* h, int32_t* rows, int32_t* cols, void* vals, 
     e.coo_cap = cap2;
   }
   // values widened to complex128 on the device: the caller's arrays are final
-  HOLO_CUDA(holo::coo_compact(e.X[e.ix], e.P, e.geom.nx, e.nzl, e.coo_offsets, e.coo_rows, e.coo_cols, nullptr,
+  HOLO_CUDA(holo::coo_compact(e.sol_volume(e.ix), e.P, e.geom.nx, e.nzl, e.coo_offsets, e.coo_rows, e.coo_cols, nullptr,
                               e.coo_vals, s));
   if ((rc = d2h_staged(e, rows, e.coo_rows, sizeof(int32_t) * tot, s))) return rc;
   if ((rc = d2h_staged(e, cols, e.coo_cols, sizeof(int32_t) * tot, s))) return rc;
@@ -1249,7 +1278,7 @@ int holo_export_coo_device(holo_handle* h, int32_t* rows, int32_t* cols, float* 
 int holo_solution_device(holo_handle* h, void** x) {
   if (!h || !x) return fail(HOLO_ERR_INVALID, "null argument");
   if (!h->e.have_solution) return fail(HOLO_ERR_INVALID, "no solution: call holo_solve first");
-  *x = h->e.X[h->e.ix];
+  *x = h->e.sol_volume(h->e.ix);
   return HOLO_OK;
 }
 
@@ -1282,6 +1311,8 @@ int holo_op_forward(holo_handle* h, const void* x, void* out, void* stream) {
     cudaStream_t s = e.st(stream);
     int rc = e.ensure_scratch();
     if (rc) return rc;
+    e.set_stack(false);  // one complex plane per local plane
+    if (e.sol_packed) e.have_solution = false;  // (its unpacked copy lives in scratch, overwritten here)
     if ((rc = e.forward_spectrum((const float2*)x, e.S[0], s))) return rc;
     HOLO_CUDA(holo::apply_mask(e.plan, e.S[0], 1, s));
     HOLO_CUDA(holo::fft_rows(e.plan, e.S[0], e.R, e.geom.ny, true, 1.0f, s));

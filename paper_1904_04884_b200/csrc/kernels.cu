@@ -206,8 +206,14 @@ constexpr bool adj_separate_stage() {
 #ifndef HOLO_ADJ_MINB
 #define HOLO_ADJ_MINB 2  // 2 CTAs / 16 warps per SM at <= 128 registers (12.48 -> 12.32 ms per 10 C3 iterations)
 #endif
-template <int N, int C, int E_>
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>::TPF <= 256 ? HOLO_ADJ_MINB : 1) k_adj_cols(const float2* __restrict__ R,
+// PK (packed real engine, see engine.cu): stack plane k holds real planes
+// j = k0 + 2k (Re) and j + 1 (Im), and its weight is U_k = c_j + i c_{j+1},
+// c = Re H = cos(phase), so that ifft2(U_k R) = ifft2(c_j R) + i ifft2(c_{j+1} R)
+// packs the two real gradients (R Hermitian).  U_k R = rA + rB with
+// rA = R H_j (1 + i G) / 2, rB = R conj(H_j) (1 + i conj G) / 2, carried from
+// stack plane to stack plane by G^2 and conj(G^2).
+template <int N, int C, int E_, bool PK = false>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 1 : (C * FftShape<N, E_>::TPF <= 256 ? HOLO_ADJ_MINB : 1)) k_adj_cols(const float2* __restrict__ R,
                                                                     const __grid_constant__ CUtensorMap out_map,
                                                                     int nx, int ny, int k0, int nzl, int ppc,
                                                                     const uint64_t* __restrict__ tab,
@@ -238,11 +244,20 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
   // (<= kMaxRecur steps: < 4e-6 relative drift worst case).
   const int kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
   float2 r[E], g[E];
+  float2 rb[PK ? E : 1];
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const uint64_t t = tab[p0 + m * st];
-    r[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(t, k0 + kb), circ));
-    g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+    if constexpr (PK) {
+      const float2 G = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+      const float2 H = cis_cycles(plane_phase(t, k0 + 2 * kb), circ), Rv = R[p0 + m * st];
+      r[m] = cmul(cmul(Rv, H), make_float2(0.5f - 0.5f * G.y, 0.5f * G.x));    // (1 + i G) / 2
+      rb[m] = cmul(cmulc(Rv, H), make_float2(0.5f + 0.5f * G.y, 0.5f * G.x));  // (1 + i conj G) / 2
+      g[m] = cmul(G, G);
+    } else {
+      r[m] = cmul(R[p0 + m * st], cis_cycles(plane_phase(t, k0 + kb), circ));
+      g[m] = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+    }
   }
 #ifndef HOLO_ADJ_UNROLL
 #define HOLO_ADJ_UNROLL 2  // alternating register roles for r / v: 12.69 -> 12.48 ms per 10 C3 iterations
@@ -253,7 +268,12 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
     float2 v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-      v[m] = r[m];
+      if constexpr (PK) {
+        v[m] = add2(r[m], rb[m]);
+        rb[m] = cmulc(rb[m], g[m]);
+      } else {
+        v[m] = r[m];
+      }
       r[m] = cmul(r[m], g[m]);
     }
     // (shared stage: the previous plane's stores must have read buf before
@@ -283,8 +303,42 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
   if (leader) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // smem outlives the reads
 }
 
+// Horner ratio of the forward plane sum, held as z.x and the pair (-z.y, z.y)
+// (acc z = swap(acc) (-z.y, z.y) + acc z.x, no sign shuffles): conj(G) for
+// the complex engine; G^2 for the packed real engine (its second sum uses
+// conj(G^2), i.e. the negated pair).
+template <bool PK>
+HD void fwd_ratio(uint64_t t, const float2* circ, float& zx, float2& zyy) {
+  const float2 g = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
+  if constexpr (PK) {
+    const float2 g2 = cmul(g, g);
+    zx = g2.x;
+    zyy = make_float2(-g2.y, g2.y);
+  } else {
+    zx = g.x;
+    zyy = make_float2(g.y, -g.y);
+  }
+}
+// Close the forward sum of a CTA whose first stack plane is kb.  Complex:
+// sum_k v_k conj(H_k) = conj(H_kb) acc.  Packed real (stack plane k = real
+// planes j = k0 + 2k, j + 1; weight conj(U_k) = c_j - i c_{j+1}): with
+// A = sum v G^(2(k-kb)) (acc) and B = sum v conj(G)^(2(k-kb)) (accb),
+// sum_k v_k conj(U_k) = [(H_j0 - i H_j1) A + (conj H_j0 - i conj H_j1) B] / 2.
+template <bool PK>
+HD float2 fwd_close(float2 acc, float2 accb, uint64_t t, int k0, int kb, const float2* circ) {
+  if constexpr (PK) {
+    const float2 h0 = cis_cycles(plane_phase(t, k0 + 2 * kb), circ);
+    const float2 h1 = cis_cycles(plane_phase(t, k0 + 2 * kb + 1), circ);
+    const float2 ca = make_float2(h0.x + h1.y, h0.y - h1.x), cb = make_float2(h0.x - h1.y, -h0.y - h1.x);
+    return mul2(add2(cmul(acc, ca), cmul(accb, cb)), splat2(0.5f));
+  } else {
+    (void)accb;
+    return cmulc(acc, cis_cycles(plane_phase(t, k0 + kb), circ));
+  }
+}
+
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
-template <int N, int C, int E_>
+template <int N, int C, int E_, bool PK = false>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const float2* __restrict__ in,
                                                                     float2* __restrict__ Spart, int nx, long long P,
                                                                     int nzl, int ppg, int k0,
@@ -303,20 +357,17 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
   const int kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
-  float2 acc[E];
+  float2 acc[E], accb[PK ? E : 1];
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
+#pragma unroll
+  for (int m = 0; m < (PK ? E : 1); ++m) accb[m] = czero();
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
   // Horner from the last plane, as in k_fwd_cols_staged
   float zx[E];
   float2 zyy[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const uint64_t t = tab[p0 + m * st];
-    const float2 g = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
-    zx[m] = g.x;
-    zyy[m] = make_float2(g.y, -g.y);
-  }
+  for (int m = 0; m < E; ++m) fwd_ratio<PK>(tab[p0 + m * st], circ, zx[m], zyy[m]);
   for (int k = ke - 1; k >= kb; --k) {
     float2 v[E];
     const float2* src = in + (long long)k * P + p0;
@@ -324,11 +375,14 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
     for (int m = 0; m < E; ++m) v[m] = src[m * st];
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
 #pragma unroll
-    for (int m = 0; m < E; ++m) acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
+    for (int m = 0; m < E; ++m) {
+      acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
+      if constexpr (PK)
+        accb[m] = fma2(swp(accb[m]), make_float2(-zyy[m].x, -zyy[m].y), fma2(accb[m], splat2(zx[m]), v[m]));
+    }
   }
 #pragma unroll
-  for (int m = 0; m < E; ++m)
-    acc[m] = cmulc(acc[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + kb), circ));
+  for (int m = 0; m < E; ++m) acc[m] = fwd_close<PK>(acc[m], accb[PK ? m : 0], tab[p0 + m * st], k0, kb, circ);
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
@@ -339,14 +393,14 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
 // shared-memory stage with 2D tensor copies while the CTA transforms plane k,
 // so the column loads leave the critical path (the plain kernel waited on HBM
 // once per plane with only 16 warps per SM to hide it).
-template <int N, int C, int E_>
 // 2 columns per CTA (128 threads) at <= 160 registers: 3 CTAs / 12 warps per
 // SM (4 columns at 190 registers fit one CTA / 8 warps: 14.5 vs 12.3 ms per 10
 // C3 iterations)
 #ifndef HOLO_FWD_MINB
 #define HOLO_FWD_MINB 3
 #endif
-__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>::TPF <= 128 ? HOLO_FWD_MINB : 1) k_fwd_cols_staged(
+template <int N, int C, int E_, bool PK = false>
+__global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftShape<N, E_>::TPF <= 128 ? HOLO_FWD_MINB : 1)) k_fwd_cols_staged(
     const __grid_constant__ CUtensorMap in_map, float2* __restrict__ Spart, int nx, long long P, int ny, int nzl,
     int ppg, int k0, const uint64_t* __restrict__ tab, const float4* __restrict__ twg,
     const float2* __restrict__ circg) {
@@ -388,9 +442,11 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
   __syncthreads();
   const int c = threadIdx.x % C, j = threadIdx.x / C;
   const int col = blockIdx.x * C + c;
-  float2 acc[E];
+  float2 acc[E], accb[PK ? E : 1];
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = czero();
+#pragma unroll
+  for (int m = 0; m < (PK ? E : 1); ++m) accb[m] = czero();
   const long long p0 = (long long)j * nx + col, st = (long long)TPF * nx;
   // sum_k v_k conj(H_k) over the CTA's planes = conj(H_kb) sum_k v_k z^(k-kb),
   // z = conj(G) = cis(-2 pi dz q) (the reference's ladder step, optics.py:146-169):
@@ -400,12 +456,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
   float zx[E];
   float2 zyy[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const uint64_t t = tab[p0 + m * st];
-    const float2 g = cis_cycles(plane_phase(t, 1) - plane_phase(t, 0), circ);
-    zx[m] = g.x;
-    zyy[m] = make_float2(g.y, -g.y);
-  }
+  for (int m = 0; m < E; ++m) fwd_ratio<PK>(tab[p0 + m * st], circ, zx[m], zyy[m]);
   for (int k = ke - 1; k >= kb; --k) {
     const int i = ke - 1 - k, b = i & 1;
     // the other stage was last read in the previous plane, before fft_line's barriers
@@ -427,12 +478,15 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, C * FftShape<N, E_>:
     for (int m = 0; m < E; ++m) v[m] = src[(j + m * TPF) * C];
     fft_line<N, false, E_>(v, j, buf + c, C, tw);
 #pragma unroll
-    for (int m = 0; m < E; ++m) acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
+    for (int m = 0; m < E; ++m) {
+      acc[m] = fma2(swp(acc[m]), zyy[m], fma2(acc[m], splat2(zx[m]), v[m]));
+      if constexpr (PK)
+        accb[m] = fma2(swp(accb[m]), make_float2(-zyy[m].x, -zyy[m].y), fma2(accb[m], splat2(zx[m]), v[m]));
+    }
   }
-  // times conj(H_kb), exact (64-bit phase)
+  // times conj(H_kb) (packed: the two-sum closure), exact (64-bit phase)
 #pragma unroll
-  for (int m = 0; m < E; ++m)
-    acc[m] = cmulc(acc[m], cis_cycles(plane_phase(tab[p0 + m * st], k0 + kb), circ));
+  for (int m = 0; m < E; ++m) acc[m] = fwd_close<PK>(acc[m], accb[PK ? m : 0], tab[p0 + m * st], k0, kb, circ);
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
@@ -543,7 +597,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
       }
       if (a.grad) {
         const float2 gg = a.grad[g];
-        y = make_float2(fmaf(-a.step, gg.x, y.x), a.real_mode ? y.y : fmaf(-a.step, gg.y, y.y));
+        y = make_float2(fmaf(-a.step, gg.x, y.x), fmaf(-a.step, gg.y, y.y));
       }
       vr[m] = y.x;
       vi[m] = y.y;
@@ -659,9 +713,9 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     }
     if (force & 1u) wr = vr[m];
     if (force & 2u) wi = vi[m];
-    if (a.real_mode) {
-      wr = fmaxf(wr - a.tau_l1, 0.f);  // solver.py:208-210: max(w - tau, 0)
-      wi = 0.f;
+    if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0), per packed real plane (Re, Im)
+      wr = fmaxf(wr - a.tau_l1, 0.f);
+      wi = fmaxf(wi - a.tau_l1, 0.f);
     } else if (a.tau_l1 > 0.f) {
       const float mag = hypotf(wr, wi);
       if (mag > a.tau_l1) {
@@ -696,7 +750,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     if (er > 0) { gyr = xr - rpr[idx - EW]; gyi = xi - rpi[idx - EW]; }
     if (ec > 0) { gxr = xr - rpr[idx - 1]; gxi = xi - rpi[idx - 1]; }
     acc[PT_TVX] += (double)sqrtf(gyr * gyr + gxr * gxr) + (double)sqrtf(gyi * gyi + gxi * gxi);
-    acc[PT_L1] += (double)hypotf(xr, xi);
+    acc[PT_L1] += a.real_mode ? (double)xr + (double)xi : (double)hypotf(xr, xi);
     const long long g = pbase + (long long)(ri0 + er) * a.nx + (rj0 + ec);
     float2 y = a.x[g];
     if (a.beta != 0.f) {
@@ -706,7 +760,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox(const ProxArgs a) {
     const float dxr = xr - y.x, dxi = xi - y.y;
     if (a.grad) {
       const float2 gg = a.grad[g];
-      acc[PT_IP] += (double)gg.x * dxr + (a.real_mode ? 0.0 : (double)gg.y * dxi);
+      acc[PT_IP] += (double)gg.x * dxr + (double)gg.y * dxi;
     }
     acc[PT_DX2] += (double)dxr * dxr + (double)dxi * dxi;
     a.xnew[g] = make_float2(xr, xi);
@@ -1118,7 +1172,7 @@ constexpr int kMaxRecur = 32;
 #endif
 #define HOLO_FWD_C(N) ((N) <= HOLO_FWD_STAGED_MAX ? HOLO_FWD_CC : 4)
 
-cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s) {
+cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed) {
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1137,9 +1191,14 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
         err = cudaErrorInvalidValue;
         return;
       }
-      err = set_smem(k_adj_cols<N, C, E>, smem);
-      k_adj_cols<N, C, E><<<grid, NT, smem, s>>>(R, map, p.nx, p.ny, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()],
-                                                  p.circle);
+      auto go = [&](auto kern) {
+        if ((err = set_smem(kern, smem))) return;
+        kern<<<grid, NT, smem, s>>>(R, map, p.nx, p.ny, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()], p.circle);
+      };
+      if (packed)
+        go(k_adj_cols<N, C, E, true>);
+      else
+        go(k_adj_cols<N, C, E>);
     };
     launch(std::integral_constant<int, HOLO_ADJ_C(N)>());  // nx >= 8 always
     COUNT_LAUNCH(1);
@@ -1156,7 +1215,8 @@ int fwd_groups(const Plan& p, int nzl) {
   return std::min(g, 64);
 }
 
-cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s) {
+cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
+                     bool packed) {
   cudaError_t err = cudaSuccess;
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
@@ -1172,14 +1232,25 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
         return;
       }
       const size_t smem = col_smem<N, C, E>(256) + sizeof(float2) * 2 * N * C;
-      err = set_smem(k_fwd_cols_staged<N, C, E>, smem);
-      k_fwd_cols_staged<N, C, E><<<grid, NT, smem, s>>>(map, Spart, p.nx, p.P, p.ny, nzl, ppg, k0, p.phase,
-                                                         p.tw_y[tw_slot<E>()], p.circle);
+      auto go = [&](auto kern) {
+        if ((err = set_smem(kern, smem))) return;
+        kern<<<grid, NT, smem, s>>>(map, Spart, p.nx, p.P, p.ny, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
+                                    p.circle);
+      };
+      if (packed)
+        go(k_fwd_cols_staged<N, C, E, true>);
+      else
+        go(k_fwd_cols_staged<N, C, E>);
     } else {
       const size_t smem = col_smem<N, C, E>(256);
-      err = set_smem(k_fwd_cols<N, C, E>, smem);
-      k_fwd_cols<N, C, E><<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
-                                                  p.circle);
+      auto go = [&](auto kern) {
+        if ((err = set_smem(kern, smem))) return;
+        kern<<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
+      };
+      if (packed)
+        go(k_fwd_cols<N, C, E, true>);
+      else
+        go(k_fwd_cols<N, C, E>);
     }
   COUNT_LAUNCH(1);
   });
@@ -1287,6 +1358,33 @@ cudaError_t load_hologram(const double* b, float2* bc, long long P, double* part
   const int g = grid_for(P, kEltThreads, 148 * 4);
   *nblocks = g;
   k_load_hologram<<<g, kEltThreads, 0, s>>>(b, bc, P, part);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+
+// packed real engine (engine.cu): zero the dummy Im part; unpack a stack of
+// nzl real planes (plane 2k = Re of stack plane k, 2k+1 = Im) to one complex
+// plane each (Im = 0)
+__global__ void k_zero_imag(float2* __restrict__ x, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i].y = 0.f;
+}
+__global__ void k_unpack_real(const float2* __restrict__ x, float2* __restrict__ out, int nzl, long long P) {
+  const long long n = (long long)((nzl + 1) / 2) * P;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long k = i / P, e = i - k * P;
+    const float2 v = x[i];
+    out[2 * k * P + e] = make_float2(v.x, 0.f);
+    if (2 * k + 1 < nzl) out[(2 * k + 1) * P + e] = make_float2(v.y, 0.f);
+  }
+}
+cudaError_t zero_imag(float2* x, long long n, cudaStream_t s) {
+  k_zero_imag<<<grid_for(n, kEltThreads, 148 * 8), kEltThreads, 0, s>>>(x, n);
+  COUNT_LAUNCH(1);
+  return cudaGetLastError();
+}
+cudaError_t unpack_real(const float2* x, float2* out, int nzl, long long P, cudaStream_t s) {
+  k_unpack_real<<<grid_for((long long)((nzl + 1) / 2) * P, kEltThreads, 148 * 8), kEltThreads, 0, s>>>(x, out, nzl, P);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

@@ -35,7 +35,7 @@ struct ProxArgs {
   int ny = 0, nx = 0, nplanes = 0;
   float beta = 0.f, step = 0.f;  // y = (1+beta) x - beta xp ; v = y - step * grad
   float tau_l1 = 0.f, tau_tv = 0.f, lr_tv = 0.f;
-  int real_mode = 0;  // real-nonnegative engine: Re(grad) only, x = max(w - tau_l1, 0), Im = 0
+  int real_mode = 0;  // packed real engine: Re / Im are two real planes, x = max(w - tau_l1, 0) per part
   int inner = 0, halo = 0, tile = 0, tiles_x = 0, tiles_per_plane = 0;
   int kind = 0;  // 0: generic tile kernel, 1: 64x64 register-strip kernel
   const float* fgp_beta = nullptr;  // [inner] FGP momentum schedule (device)
@@ -91,9 +91,11 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
                      cudaStream_t s);
 // adjoint column pass: out[k] = colIFFT(H_{k0+k} * R), k < nzl (R already band-masked)
-cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s);
+cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s,
+                     bool packed = false);  // packed: the packed real engine's stack (engine.cu)
 // forward column pass: Spart[g] = sum_{k in group g} colFFT(in[k]) * conj(H_{k0+k})
-cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s);
+cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
+                     bool packed = false);
 int fwd_groups(const Plan& p, int nzl);
 cudaError_t sum_groups(const Plan& p, const float2* Spart, int groups, float2* S, cudaStream_t s);
 
@@ -127,6 +129,8 @@ cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplane
 // b (fp64, host layout) -> fp32 complex plane (imag 0), per-block sum b^2
 cudaError_t load_hologram(const double* b, float2* bc, long long P, double* part, int* nblocks, cudaStream_t s);
 // real part extraction with scale (for forward-operator output)
+cudaError_t zero_imag(float2* x, long long n, cudaStream_t s);
+cudaError_t unpack_real(const float2* x, float2* out, int nzl, long long P, cudaStream_t s);
 cudaError_t real_part(const float2* in, float* out, long long n, float scale, cudaStream_t s);
 cudaError_t real_to_complex(const float* in, float2* out, long long n, cudaStream_t s);
 // mask a spectrum in place (m = 0 -> 0)

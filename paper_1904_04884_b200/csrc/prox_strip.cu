@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -284,7 +285,9 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
 // EDGE: the region touches a plane edge, so its outer rows/columns need the
 // exact replicated-edge rule; otherwise they are garbage zone and the
 // lane-0 / lane-31 / band-0 / band-(NW-1) selects are skipped.
-template <bool TV, bool EDGE, int PH>
+// RM: the packed real engine (x = max(w - tau, 0) per part), a separate
+// instantiation so the complex kernels carry no real-mode branch
+template <bool TV, bool EDGE, int PH, bool RM>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
                                           unsigned& bph, float4* pre, uint64_t* sbar, int work, const Work& wk,
                                           int next_work, const GeoSlot* nxgeo, float4* stage, float4* save,
@@ -389,8 +392,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         y1 = fma2(cb, y1, mul2(cm, hi2(o)));
       }
       if (a.grad) {
-        float4 gg = slot(2, s);
-        if (a.real_mode) gg.y = gg.w = 0.f;  // real engine: Re(grad) only
+        const float4 gg = slot(2, s);
         y0 = fma2(cs, lo2(gg), y0);
         y1 = fma2(cs, hi2(gg), y1);
       }
@@ -445,9 +447,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const float wr = rp[s][k].x, wi = rp[s][k].y;
-      if (a.real_mode) {  // solver.py:208-210: max(w - tau, 0)
-        p[s][k] = make_float2(fmaxf(wr - tl, 0.f), 0.f);
-        l1 += p[s][k].x;
+      if constexpr (RM) {  // solver.py:208-210: max(w - tau, 0), per packed real plane (Re, Im)
+        p[s][k] = make_float2(fmaxf(wr - tl, 0.f), fmaxf(wi - tl, 0.f));
+        l1 += p[s][k].x + p[s][k].y;
         continue;
       }
       const float n2 = fmaf(wr, wr, wi * wi);
@@ -771,7 +773,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         }
         float4 gr4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (a.grad) gr4 = staged ? slot(2, s) : *reinterpret_cast<const float4*>(a.grad + g);
-        if (a.real_mode) gr4.y = gr4.w = 0.f;
         const float2 gr[2] = {lo2(gr4), hi2(gr4)};
         const float2 dx0 = sub2(p[s][0], y[0]), dx1 = sub2(p[s][1], y[1]);
         const float2 ip = fma2(gr[0], dx0, mul2(gr[1], dx1));  // (re, im) parts of <g, dx>
@@ -828,7 +829,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
-template <bool TV, int PH>
+template <bool TV, int PH, bool RM = false>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(NT <= 1024, "");
   // Bands, then the staged slots: [2][x, x_prev, grad] (single pass), or the
@@ -899,10 +900,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
     if (cur.edge)
-      prox_tile<TV, true, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+      prox_tile<TV, true, PH, RM>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
                               &bars[sb ^ 1]);
     else
-      prox_tile<TV, false, PH>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+      prox_tile<TV, false, PH, RM>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
                                &bars[sb ^ 1]);
     work = nw;
   }
@@ -1020,21 +1021,28 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
     kern<<<grid, NT, smem, s>>>(a, maps);
   };
   if (a.tau_tv > 0.f && a.pass_len && !a.walk) return cudaErrorInvalidValue;  // multi-pass kinds walk strips
-  if (a.tau_tv > 0.f && a.pass_len) {
-    if (a.t0 == 0)
-      launch(k_prox_strip<true, 1>);
-    else if (a.t1 >= a.inner)
-      launch(k_prox_strip<true, 3>);
-    else
-      launch(k_prox_strip<true, 2>);
-  } else if (a.tau_tv > 0.f) {
-    launch(k_prox_strip<true, 0>);
-  } else {
-    if (a.walk)  // no TV: no FGP passes, but the strip-walk tiling of this setup
-      launch(k_prox_strip<false, 1>);
-    else
-      launch(k_prox_strip<false, 0>);
-  }
+  auto pick = [&](auto rm) {
+    constexpr bool RM = decltype(rm)::value;
+    if (a.tau_tv > 0.f && a.pass_len) {
+      if (a.t0 == 0)
+        launch(k_prox_strip<true, 1, RM>);
+      else if (a.t1 >= a.inner)
+        launch(k_prox_strip<true, 3, RM>);
+      else
+        launch(k_prox_strip<true, 2, RM>);
+    } else if (a.tau_tv > 0.f) {
+      launch(k_prox_strip<true, 0, RM>);
+    } else {
+      if (a.walk)  // no TV: no FGP passes, but the strip-walk tiling of this setup
+        launch(k_prox_strip<false, 1, RM>);
+      else
+        launch(k_prox_strip<false, 0, RM>);
+    }
+  };
+  if (a.real_mode)
+    pick(std::true_type());
+  else
+    pick(std::false_type());
   if (e) return e;
   return cudaGetLastError();
 }

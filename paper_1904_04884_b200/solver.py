@@ -9,11 +9,12 @@ Differences a caller can observe (documented in DESIGN.md):
     ``cfg.dtype`` says (the north-star parity bar is rel-L2 <= 1e-4 in fp32);
   * ``dense_plane_budget`` is accepted and ignored: the whole volume is
     resident in HBM (it only bounded host memory in the reference);
-  * ``real_nonnegative=True`` runs the same complex kernels restricted to real
-    volumes (the real engine's operators are the complex ones on real x, with
-    Re() of the adjoint), not the reference's half-spectrum rfft layout; its
-    step estimate replays the reference's power iteration (same
-    ``default_rng(0)`` start vector, generated on the host) on the GPU.
+  * ``real_nonnegative=True`` packs two real planes into one complex stack
+    plane (Re / Im) and runs the complex kernels on half as many planes with
+    the cosine weights c_2k + i c_2k+1 -- the same operator as the reference's
+    half-spectrum rfft layout; its step estimate replays the
+    reference's power iteration (same ``default_rng(0)`` start vector,
+    generated on the host) on the GPU.
 """
 
 from __future__ import annotations
