@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   // strip walk: strips blockIdx.x, +gridDim.x, ..., each region by region
   const int nstrips = a.tiles_x * a.nplanes;
   auto strip_from = [&](int st) {
-    if (a.force)
+    if (!FAST && a.force)
       while (st < nstrips && !a.force[fdiv(st, a.tiles_x, a.rcp_tx)]) st += gridDim.x;
     return st < nstrips ? st * a.ky : -1;
   };
@@ -1029,10 +1029,11 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
   auto pick = [&](auto rm) {
     constexpr bool RM = decltype(rm)::value;
     if (a.tau_tv > 0.f && a.pass_len) {
+      const bool fast = !a.ipdx && !a.force;
       if (a.t0 == 0)
-        launch(k_prox_strip<true, 1, RM>);
+        launch(k_prox_strip<true, 1, RM>);  // (no force / ipdx code in a first pass)
       else if (a.t1 >= a.inner)
-        launch(k_prox_strip<true, 3, RM>);
+        fast ? launch(k_prox_strip<true, 3, RM, true>) : launch(k_prox_strip<true, 3, RM>);
       else
         launch(k_prox_strip<true, 2, RM>);
     } else if (a.tau_tv > 0.f) {
