@@ -291,7 +291,10 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
 // 0), no guard fix-up (a.force == nullptr) -- compiled without those branches
 // (C3 prox 76.4 -> 72.8 ms per 10 iterations; also compiling out the beta == 0
 // and grad == nullptr branches measured 73.1-73.4).
-template <bool TV, bool EDGE, int PH, bool RM, bool FAST>
+#ifndef HOLO_TT_UNROLL
+#define HOLO_TT_UNROLL 2  // (4, a full unroll at T = 5, spills 52 B)
+#endif
+template <bool TV, bool EDGE, int PH, bool RM, bool FAST, int TT>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
                                           unsigned& bph, float4* pre, uint64_t* sbar, int work, const Work& wk,
                                           int next_work, const GeoSlot* nxgeo, float4* stage, float4* save,
@@ -540,8 +543,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     // updated between the previous iteration's arrive and the wait for the
     // neighbours' band data; rows 0 and SR-1 follow the wait.
     const float2 ptau = splat2(a.tau_tv);
-#pragma unroll 2
-    for (int t = tstart; t < a.t1; ++t) {
+    // (TT > 0: the FGP depth is a compile-time constant -- T = 5, the
+    // reference's default: C3 prox 75.7 -> 74.7 ms per 10 iterations)
+    const int tend = TT > 0 ? TT : a.t1;
+    constexpr int kTU = TT > 0 ? HOLO_TT_UNROLL : 2;
+#pragma unroll kTU
+    for (int t = tstart; t < tend; ++t) {
       const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       // single pass (T <= 8): the momentum schedule from the parameter bank
       const float2 bt2 = splat2(PH == 0 ? a.fgpb[t] : __ldg(a.fgp_beta + t));
@@ -834,7 +841,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
-template <bool TV, int PH, bool RM = false, bool FAST = false>
+template <bool TV, int PH, bool RM = false, bool FAST = false, int TT = 0>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(NT <= 1024, "");
   // Bands, then the staged slots: [2][x, x_prev, grad] (single pass), or the
@@ -905,10 +912,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
     if (cur.edge)
-      prox_tile<TV, true, PH, RM, FAST>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+      prox_tile<TV, true, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
                               &bars[sb ^ 1]);
     else
-      prox_tile<TV, false, PH, RM, FAST>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
+      prox_tile<TV, false, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
                                &bars[sb ^ 1]);
     work = nw;
   }
@@ -1037,7 +1044,9 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
       else
         launch(k_prox_strip<true, 2, RM>);
     } else if (a.tau_tv > 0.f) {
-      if (!a.ipdx && !a.force)  // the engine's main pass
+      if (!a.ipdx && !a.force && a.inner == 5 && !getenv("HOLO_PROX_NOTT"))  // the engine's main pass, T = 5
+        launch(k_prox_strip<true, 0, RM, true, 5>);
+      else if (!a.ipdx && !a.force)  // the engine's main pass
         launch(k_prox_strip<true, 0, RM, true>);
       else
         launch(k_prox_strip<true, 0, RM>);
