@@ -59,6 +59,10 @@ struct ProxArgs {
   float4* rbuf = nullptr;            // extrapolated (rp, rq) per pixel, two halves
   long long sstride = 0;             // elements per half: pass i writes half i&1, reads (i-1)&1
   float* tvv = nullptr;              // per-tile TV(v) partials [tile][2], first pass -> last pass
+  // strip kernel, single pass: tiles [ix0, ix1) x [iy0, iy1) are interior (their
+  // regions touch no plane edge); ordered launches visit those first
+  int ix0 = 0, ix1 = 0, iy0 = 0, iy1 = 0, icnt = 0;
+  float rcp_icnt = 0.f, rcp_ecnt = 0.f, rcp_nix = 0.f, rcp_ew = 0.f;
 };
 
 // Peer-memory spectrum reduction (peer.cu): every rank's symmetric buffers.

@@ -149,11 +149,44 @@ HD Work work_geom(const ProxArgs& a, int work) {
   return wk;
 }
 
+// Ordered visit (single pass, ORD): local index lw < nplanes * icnt walks the
+// interior tiles plane by plane (row-major inside the interior rectangle),
+// the rest the edge ring, so a CTA runs the interior instantiation and then
+// the edge one instead of alternating between the two code copies.
+template <bool ORD>
+HD int ordered_work(const ProxArgs& a, int lw) {
+  if constexpr (!ORD) return lw;
+  const int ni = a.icnt * a.nplanes, nix = a.ix1 - a.ix0;
+  int plane, r, tile;
+  if (lw < ni) {
+    plane = fdiv(lw, a.icnt, a.rcp_icnt);
+    r = lw - plane * a.icnt;
+    const int ry = fdiv(r, nix, a.rcp_nix);
+    tile = (a.iy0 + ry) * a.tiles_x + a.ix0 + r - ry * nix;
+  } else {
+    const int ecnt = a.tiles_per_plane - a.icnt;
+    lw -= ni;
+    plane = fdiv(lw, ecnt, a.rcp_ecnt);
+    r = lw - plane * ecnt;
+    const int top = a.iy0 * a.tiles_x, ew = a.tiles_x - nix, mid = (a.iy1 - a.iy0) * ew;
+    if (r < top) {
+      tile = r;
+    } else if (r - top < mid) {
+      r -= top;
+      const int ry = fdiv(r, ew, a.rcp_ew), c = r - ry * ew;
+      tile = (a.iy0 + ry) * a.tiles_x + (c < a.ix0 ? c : c + nix);
+    } else {
+      tile = a.iy1 * a.tiles_x + r - top - mid;
+    }
+  }
+  return plane * a.tiles_per_plane + tile;
+}
+
 // The leader computes the next region's geometry anyway (for its TMA copies)
 // and publishes it in shared memory; the other 511 threads read it instead of
 // repeating the divisions.
 struct GeoSlot {
-  int plane, i0, i1, j0, j1, ri0, rj0, k, rsave, pad[3];
+  int plane, i0, i1, j0, j1, ri0, rj0, k, rsave, work, pad[2];  // work: global index (ordered visits)
 };
 HD void geo_store(GeoSlot& g, const Work& wk) {
   g.plane = wk.plane;
@@ -841,7 +874,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
 
 // Persistent: one CTA per SM walks regions blockIdx.x, +gridDim.x, ...
 // (fix-up pass: only regions of planes whose guard fired).
-template <bool TV, int PH, bool RM = false, bool FAST = false, int TT = 0>
+template <bool TV, int PH, bool RM = false, bool FAST = false, int TT = 0, bool ORD = false>
 __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __grid_constant__ TmaMaps maps) {
   static_assert(NT <= 1024, "");
   // Bands, then the staged slots: [2][x, x_prev, grad] (single pass), or the
@@ -883,7 +916,8 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     mbar_init(&bbar[0], NW);
     mbar_init(&bbar[1], NW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    geo_store(geo[0], work_geom<WALK>(a, work));
+    geo_store(geo[0], work_geom<WALK>(a, ordered_work<ORD>(a, work)));
+    if (ORD) geo[0].work = ordered_work<ORD>(a, work);
   }
   __syncthreads();
   if (leader) {
@@ -901,8 +935,10 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     const int nw = next_of(work);
     // geo[buf ^ 1] and the other slot were last read by the previous region, before its final barrier
     if (leader && nw >= 0) {
-      const Work wn = work_geom<WALK>(a, nw);
+      const int gw = ordered_work<ORD>(a, nw);
+      const Work wn = work_geom<WALK>(a, gw);
       geo_store(geo[buf ^ 1], wn);
+      if (ORD) geo[buf ^ 1].work = gw;
       if (staged) tma_region_walk(a, maps, pre + (buf ^ 1) * 2 * kSlotF4, &bars[buf ^ 1], wn);
     }
     const Work cur = geo_load<WALK>(a, geo[buf]);
@@ -911,12 +947,13 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
     float4* slot = pre + sb * 2 * kSlotF4;  // (later passes: the state slot at pre)
     mbar_wait(&bars[sb], (phase >> sb) & 1u);
     phase ^= 1u << sb;
+    const int gwork = ORD ? geo[buf].work : work;
     if (cur.edge)
-      prox_tile<TV, true, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
-                              &bars[sb ^ 1]);
+      prox_tile<TV, true, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], gwork, cur, nw, &geo[buf ^ 1], pre,
+                                            save, &bars[sb ^ 1]);
     else
-      prox_tile<TV, false, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], work, cur, nw, &geo[buf ^ 1], pre, save,
-                               &bars[sb ^ 1]);
+      prox_tile<TV, false, PH, RM, FAST, TT>(a, maps, sm, bbar, bph, slot, &bars[0], gwork, cur, nw, &geo[buf ^ 1], pre,
+                                             save, &bars[sb ^ 1]);
     work = nw;
   }
 }
@@ -997,6 +1034,29 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.rcp_tx = 1.f / (float)a.tiles_x;
   a.rcp_tpp = 1.f / (float)a.tiles_per_plane;
   a.part_warps = NW;
+  // interior tile rectangle (single pass): region frames clear of every plane edge
+  auto interior = [](int n_tiles, int tile, int halo, int n, int R, int& t0, int& t1) {
+    t0 = t1 = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int r0 = t * tile - halo;
+      if (r0 > 0 && r0 < n - R) {
+        if (t1 == t0) t0 = t;
+        t1 = t + 1;
+      }
+    }
+  };
+  a.icnt = 0;
+  if (!a.walk) {
+    interior(a.tiles_x, a.tile, a.halo, nx, RW, a.ix0, a.ix1);
+    interior(a.ky, a.tile_h, a.halo, ny, RH, a.iy0, a.iy1);
+    a.icnt = (a.ix1 - a.ix0) * (a.iy1 - a.iy0);
+  }
+  if (a.icnt > 0) {
+    a.rcp_icnt = 1.f / (float)a.icnt;
+    a.rcp_ecnt = 1.f / (float)(a.tiles_per_plane - a.icnt);
+    a.rcp_nix = 1.f / (float)(a.ix1 - a.ix0);
+    a.rcp_ew = 1.f / (float)(a.tiles_x - (a.ix1 - a.ix0));
+  }
 }
 
 cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
@@ -1044,7 +1104,9 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
       else
         launch(k_prox_strip<true, 2, RM>);
     } else if (a.tau_tv > 0.f) {
-      if (!a.ipdx && !a.force && a.inner == 5 && !getenv("HOLO_PROX_NOTT"))  // the engine's main pass, T = 5
+      if (!a.ipdx && !a.force && a.inner == 5 && a.icnt > 0 && !getenv("HOLO_PROX_NOORD"))
+        launch(k_prox_strip<true, 0, RM, true, 5, true>);  // the engine's main pass, T = 5
+      else if (!a.ipdx && !a.force && a.inner == 5 && !getenv("HOLO_PROX_NOTT"))
         launch(k_prox_strip<true, 0, RM, true, 5>);
       else if (!a.ipdx && !a.force)  // the engine's main pass
         launch(k_prox_strip<true, 0, RM, true>);
