@@ -34,6 +34,7 @@ __global__ void k(float2* out, float s, int iters, long long* cyc) {
       if (MODE == 7) a[i] = add2(a[i], cr);                                // FADD2 per-thread registers
     }
   }
+  __syncthreads();  // every warp's loop inside the timed span
   long long t1 = clock64();
   float2 acc = make_float2(0, 0);
   for (int i = 0; i < 8; ++i) acc = add2(acc, a[i]);
