@@ -303,13 +303,20 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(kStateBytes)
                : "memory");
-  const int off[3] = {kStateV, kStateS, kStateR}, c0[3] = {2 * wk.tg.rj0, 4 * wk.tg.rj0, 4 * wk.tg.rj0};
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(slot + kStateV)),
+      "l"(reinterpret_cast<uint64_t>(&maps.m[0])), "r"(2 * wk.tg.rj0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+  // dual state: rows split by column parity (even columns, then odd; see the
+  // last-pass stores), one 3-D box {32 pixels, both parities, RH rows} each
+  const int off[2] = {kStateS, kStateR};
 #pragma unroll
-  for (int k = 0; k < 3; ++k)
+  for (int k = 0; k < 2; ++k)
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
             smem_u32(slot + off[k])),
-        "l"(reinterpret_cast<uint64_t>(&maps.m[k])), "r"(c0[k]), "r"(c1), "r"(smem_u32(bar))
+        "l"(reinterpret_cast<uint64_t>(&maps.m[k + 1])), "r"(2 * wk.tg.rj0), "r"(0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -411,7 +418,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       v[s][1] = hi2(vv);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const float4 sq = pre[kStateS + row * RW + 2 * lane + k], rr = pre[kStateR + row * RW + 2 * lane + k];
+        // [row][column parity][lane] (see tma_state)
+        const float4 sq = pre[kStateS + row * RW + k * 32 + lane], rr = pre[kStateR + row * RW + k * 32 + lane];
         p[s][k] = lo2(sq);
         q[s][k] = hi2(sq);
         rp[s][k] = lo2(rr);
@@ -645,10 +653,16 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       for (int s = 0; s < SR; ++s) {
         const long long g = g0 + (long long)s * a.nx;
         if (!(rInt & (1u << s)) || !cInt) continue;
+#ifdef HOLO_EXP_NOSTORE  // timing experiment only (HOLO_EXP_NOSTORE = 2: middle passes, 3: all)
+        if (PH == 2 || HOLO_EXP_NOSTORE == 3) continue;
+#endif
+        // parity-split rows (even columns, then odd): a warp's store is 512
+        // contiguous bytes instead of every other 16 bytes of 1 KB
+        const long long gs = (pass & 1) * a.sstride + g - (gj >> 1);  // row start + gj / 2
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          a.sbuf[(pass & 1) * a.sstride + g + k] = f4(p[s][k], q[s][k]);
-          a.rbuf[(pass & 1) * a.sstride + g + k] = f4(rp[s][k], rq[s][k]);
+          a.sbuf[gs + k * (a.nx >> 1)] = f4(p[s][k], q[s][k]);
+          a.rbuf[gs + k * (a.nx >> 1)] = f4(rp[s][k], rq[s][k]);
         }
         if (first) *reinterpret_cast<float4*>(a.vbuf + g) = f4(v[s][0], v[s][1]);
       }
@@ -979,6 +993,29 @@ CUresult encode_map(CUtensorMap* m, const void* base, int ny_total, int nx, int 
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+// Dual-state arrays (float4 per pixel): every row stored as its even columns
+// then its odd columns; viewed as [rows][parity][nx/2] float4 with boxes of
+// {32 pixels, 2 parities, RH rows}, which land in shared memory as
+// [row][parity][32] -- lane l's two pixels at (row, 0, l) and (row, 1, l).
+CUresult encode_state_map(CUtensorMap* m, const void* base, int ny_total, int nx) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return CUDA_ERROR_NOT_FOUND;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * nx, 2, (cuuint64_t)ny_total};  // floats: 4 per pixel, nx/2 pixels
+  const cuuint64_t strides[2] = {(cuuint64_t)2 * nx * sizeof(float), (cuuint64_t)4 * nx * sizeof(float)};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * RW), 2, RH};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 }  // namespace
 
 int prox_strip_max_halo() { return 14; }
@@ -1079,8 +1116,8 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s) {
   } else {  // later passes: v and the dual state half written by the previous pass
     const long long half = ((a.t0 / a.pass_len - 1) & 1) * a.sstride;
     if (encode_map(&maps.m[0], a.vbuf, rows, a.nx) != CUDA_SUCCESS ||
-        encode_map(&maps.m[1], a.sbuf + half, rows, a.nx, 4) != CUDA_SUCCESS ||
-        encode_map(&maps.m[2], a.rbuf + half, rows, a.nx, 4) != CUDA_SUCCESS)
+        encode_state_map(&maps.m[1], a.sbuf + half, rows, a.nx) != CUDA_SUCCESS ||
+        encode_state_map(&maps.m[2], a.rbuf + half, rows, a.nx) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   const long long total = a.walk ? (long long)a.tiles_x * a.nplanes  // strips
