@@ -587,7 +587,10 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     // (TT > 0: the FGP depth is a compile-time constant -- T = 5, the
     // reference's default: C3 prox 75.7 -> 74.7 ms per 10 iterations)
     const int tend = TT > 0 ? TT : a.t1;
-    constexpr int kTU = TT > 0 ? HOLO_TT_UNROLL : 2;
+    // multi-pass kernels, per pass kind (C5 passes, ncu per launch, unroll 1 / 2 / 3):
+    // first 12.7 / 15.4 / 14.7 ms (168 B of spills at 2), middle 11.6 / 11.0 / 11.5,
+    // last 12.3 / 10.9 / 10.7
+    constexpr int kTU = TT > 0 ? HOLO_TT_UNROLL : (PH == 1 ? 1 : PH == 3 ? 3 : 2);
 #pragma unroll kTU
     for (int t = tstart; t < tend; ++t) {
       const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
@@ -653,9 +656,6 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       for (int s = 0; s < SR; ++s) {
         const long long g = g0 + (long long)s * a.nx;
         if (!(rInt & (1u << s)) || !cInt) continue;
-#ifdef HOLO_EXP_NOSTORE  // timing experiment only (HOLO_EXP_NOSTORE = 2: middle passes, 3: all)
-        if (PH == 2 || HOLO_EXP_NOSTORE == 3) continue;
-#endif
         // parity-split rows (even columns, then odd): a warp's store is 512
         // contiguous bytes instead of every other 16 bytes of 1 KB
         const long long gs = (pass & 1) * a.sstride + g - (gj >> 1);  // row start + gj / 2
