@@ -34,11 +34,13 @@ for r in rows:
     if hdr and r and r[0].startswith("0x"):
         blocks[-1][1].append((int(r[0], 16), int(r[hdr["Warp Stall Sampling (All Samples)"]] or 0), int(r[hdr["Instructions Executed"]] or 0)))
 for name, data in blocks:
-    m = re.search(r"k_prox_strip<\(bool\)(\d), \(int\)(\d)>", name) or re.search(r"k_prox_strip<(\d), (\d)>", name)
+    args = re.search(r"k_prox_strip<([^>]*)>", name)
     key = None
-    if m:
-        tv, ph = m.group(1), m.group(2)
-        key = [k for k in maps if f"k_prox_stripILb{tv}ELi{ph}E" in k]
+    if args:
+        v = [re.sub(r"\(\w+\)", "", x).strip() for x in args.group(1).split(",")]
+        kinds = ["b", "i", "b", "b", "i", "b"]  # TV, PH, RM, FAST, TT, ORD
+        mang = "".join(f"L{k}{x}E" for k, x in zip(kinds, v))
+        key = [k for k in maps if f"k_prox_stripI{mang}" in k]
     if not key: print("no map for", name[:60]); continue
     amap = maps[key[0]]; base = data[0][0]
     acc = collections.defaultdict(lambda: [0, 0])

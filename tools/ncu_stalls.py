@@ -2,7 +2,7 @@
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 import os
-k = ["-k", "regex:" + os.environ["NCU_K"]] if os.environ.get("NCU_K") else []  # one kernel of a multi-kernel report
+k = (["-k", "regex:" + os.environ["NCU_K"]] + (["--kernel-name-base", "mangled"] if os.environ.get("NCU_MANGLED") else [])) if os.environ.get("NCU_K") else []  # one kernel of a multi-kernel report
 txt = subprocess.run(["ncu", "-i", rep] + k + ["--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 hdr = rows[1]; ix = {h: i for i, h in enumerate(hdr)}
