@@ -365,6 +365,7 @@ struct Engine {
   uint8_t* force_acc = nullptr; // [nzl]
   float* fgp_beta = nullptr;
   int fgp_cap = 0;
+  int fgp_inner = -1;  // depth whose momentum schedule fgp_beta holds
   // multi-pass FGP state (large T): v, 2 halves of (p,q) and (rp,rq), per-tile TV(v)
   float2* mp_v = nullptr;
   float4* mp_s = nullptr;
@@ -518,6 +519,7 @@ struct Engine {
       fgp_beta = nullptr;
       HOLO_CUDA(cudaMalloc(&fgp_beta, sizeof(float) * inner));
       fgp_cap = inner;
+      fgp_inner = -1;
     }
     // data-independent FGP momentum (prox.py:132-133)
     std::vector<float> bt(inner);
@@ -528,8 +530,11 @@ struct Engine {
       t = tn;
     }
     for (int i = 0; i < inner && i < 16; ++i) a.fgpb[i] = bt[i];
-    HOLO_CUDA(cudaMemcpyAsync(fgp_beta, bt.data(), sizeof(float) * inner, cudaMemcpyHostToDevice, s));
-    HOLO_CUDA(cudaStreamSynchronize(s));  // bt is a stack buffer
+    if (inner != fgp_inner) {  // once per depth: no stream sync on every attempt
+      HOLO_CUDA(cudaMemcpyAsync(fgp_beta, bt.data(), sizeof(float) * inner, cudaMemcpyHostToDevice, s));
+      HOLO_CUDA(cudaStreamSynchronize(s));  // bt is a stack buffer
+      fgp_inner = inner;
+    }
     a.fgp_beta = fgp_beta;
     return HOLO_OK;
   }
