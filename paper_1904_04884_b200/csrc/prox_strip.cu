@@ -332,7 +332,7 @@ HD void tma_state(const ProxArgs& a, const TmaMaps& maps, float4* slot, uint64_t
 // (C3 prox 76.4 -> 72.8 ms per 10 iterations; also compiling out the beta == 0
 // and grad == nullptr branches measured 73.1-73.4).
 #ifndef HOLO_TT_UNROLL
-#define HOLO_TT_UNROLL 2  // (4, a full unroll at T = 5, spills 52 B)
+#define HOLO_TT_UNROLL 3  // (C3 prox 74.0 -> 73.4 ms per 10 iterations vs 2; 4, a full unroll at T = 5, spills 48 B)
 #endif
 template <bool TV, bool EDGE, int PH, bool RM, bool FAST, int TT>
 __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps, Bands& sm, uint64_t* bbar,
