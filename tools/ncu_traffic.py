@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 # NCU_K=<regex>: one kernel of a multi-kernel report
-_K = ["-k", "regex:" + os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+_K = ((["-k", "regex:" + os.environ["NCU_K"]] + (["--kernel-name-base", "mangled"] if os.environ.get("NCU_MANGLED") else []))
+      if os.environ.get("NCU_K") else [])
 
 rep, cls, vox = sys.argv[1], sys.argv[2], int(sys.argv[3])
 out = sys.argv[4] if len(sys.argv) > 4 else os.path.join(os.path.dirname(__file__), "..", "profiles", "r01_traffic.json")
