@@ -141,6 +141,9 @@ constexpr int row_tw_f2() {
   return N >= 2048 ? tw_f2<N, E>() : 2 * N;
 }
 
+#ifndef HOLO_ROW_PF_DIST
+#define HOLO_ROW_PF_DIST 1  // row groups ahead (grid strides) prefetched into L2 (2: 14.0-15.0, 3: 15.0-15.8 ms)
+#endif
 template <int N, bool INV, int E_>
 __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
                                                           long long nrows, float scale, const float4* __restrict__ twg) {
@@ -160,6 +163,19 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
     const float2* src = in + row * N + j;
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = active ? src[m * TPF] : czero();
+    // the next row group (contiguous rows) into L2 while this one transforms:
+    // the loads above only start once the previous group is written, and with
+    // 2-4 CTAs per SM the HBM queue runs dry during the FFTs (C3 row passes
+    // 14.48 -> 12.83 ms per 10 iterations, C4's 2048-point rows 26.4 -> 20.4)
+    if (threadIdx.x == 0) {
+      const long long nr0 = row0 + (long long)HOLO_ROW_PF_DIST * gridDim.x * RPC;
+      if (nr0 < nrows) {
+        const long long cnt = nrows - nr0 < RPC ? nrows - nr0 : RPC;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(in + nr0 * N),
+                     "r"((unsigned)(cnt * N * sizeof(float2)))
+                     : "memory");
+      }
+    }
     fft_line<N, INV, E_>(v, j, buf + lr * Sh::PADN, 1, tw);
     if (active) {
       float2* dst = out + row * N + j;
