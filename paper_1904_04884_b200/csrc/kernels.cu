@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 1 : (C * FftSha
 #ifndef HOLO_ADJ_UNROLL
 #define HOLO_ADJ_UNROLL 2  // alternating register roles for r / v: 12.69 -> 12.48 ms per 10 C3 iterations
 #endif
-  constexpr int kUnroll = HOLO_ADJ_UNROLL;
+  constexpr int kUnroll = E_ >= 32 ? 1 : HOLO_ADJ_UNROLL;  // (radix-32 columns: 236 registers at 1, 254 at 2)
 #pragma unroll kUnroll
   for (int k = kb; k < ke; ++k) {
     float2 v[E];
@@ -1192,9 +1192,13 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
-    constexpr int E = DefaultE<N>::value;  // radix-32 columns measured slower (occupancy)
-    auto launch = [&](auto cc) {
+    // 512- and 1024-point columns of the complex engine: radix-32 (one shared-memory
+    // exchange and one table-twiddle pass instead of two; 236 registers, 2 CTAs of
+    // 128 threads per SM): C3 adjoint columns 10.97 -> 9.58 ms per 10 iterations.
+    // The packed real engine carries a second recurrence (rb[]) and keeps radix 16.
+    auto launch = [&](auto cc, auto ee) {
       constexpr int C = decltype(cc)::value;  // C x 8-byte row segments per warp load / store
+      constexpr int E = decltype(ee)::value;
       constexpr int NT = C * FftShape<N, E>::TPF;
       const size_t smem =
           col_smem<N, C, E>(256) + (adj_separate_stage<N, C, E>() ? sizeof(float2) * ((size_t)N * C + 16) : 0);
@@ -1211,12 +1215,20 @@ cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k
         if ((err = set_smem(kern, smem))) return;
         kern<<<grid, NT, smem, s>>>(R, map, p.nx, p.ny, k0, nzl, ppc, p.phase, p.tw_y[tw_slot<E>()], p.circle);
       };
-      if (packed)
-        go(k_adj_cols<N, C, E, true>);
-      else
+      if constexpr (E == DefaultE<N>::value) {
+        if (packed)
+          go(k_adj_cols<N, C, E, true>);
+        else
+          go(k_adj_cols<N, C, E>);
+      } else {
         go(k_adj_cols<N, C, E>);
+      }
     };
-    launch(std::integral_constant<int, HOLO_ADJ_C(N)>());  // nx >= 8 always
+    constexpr int E32 = (N == 512 || N == 1024) ? 32 : DefaultE<N>::value;
+    if (!packed && E32 == 32 && !std::getenv("HOLO_ADJ_E16"))
+      launch(std::integral_constant<int, HOLO_ADJ_C(N)>(), std::integral_constant<int, E32>());  // nx >= 8 always
+    else
+      launch(std::integral_constant<int, HOLO_ADJ_C(N)>(), std::integral_constant<int, DefaultE<N>::value>());
     COUNT_LAUNCH(1);
   });
   if (!ok) return cudaErrorInvalidValue;
