@@ -596,6 +596,9 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       // single pass (T <= 8): the momentum schedule from the parameter bank
       const float2 bt2 = splat2(PH == 0 ? a.fgpb[t] : __ldg(a.fgp_beta + t));
+      // final step of a single pass: the epilogue reads only p, q, so the
+      // extrapolated duals, the band's X and its band-top rp are not formed
+      const bool fin = PH == 0 && t == tend - 1;
       // one row's dual update from its u, given the u of the row above
       auto update = [&](int s, float2 u0, float2 u1, float2 up0, float2 up1) {
         float2 gx0, gx1;
@@ -605,10 +608,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         float2 pn1 = fma2(lr2, gy1, rp[s][1]), qn1 = fma2(lr2, gx1, rq[s][1]);
         project(pn0, qn0);
         project(pn1, qn1);
-        rp[s][0] = fma2(bt2, sub2(pn0, p[s][0]), pn0);
-        rq[s][0] = fma2(bt2, sub2(qn0, q[s][0]), qn0);
-        rp[s][1] = fma2(bt2, sub2(pn1, p[s][1]), pn1);
-        rq[s][1] = fma2(bt2, sub2(qn1, q[s][1]), qn1);
+        if (!fin) {
+          rp[s][0] = fma2(bt2, sub2(pn0, p[s][0]), pn0);
+          rq[s][0] = fma2(bt2, sub2(qn0, q[s][0]), qn0);
+          rp[s][1] = fma2(bt2, sub2(pn1, p[s][1]), pn1);
+          rq[s][1] = fma2(bt2, sub2(qn1, q[s][1]), qn1);
+        }
         p[s][0] = pn0;
         q[s][0] = qn0;
         p[s][1] = pn1;
@@ -639,9 +644,11 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         update(0, u[0][0], u[0][1], up0, up1);
       }
       update(SR - 1, fma2(ptau, lo2(d4), xl0), fma2(ptau, hi2(d4), xl1), u[SR - 2][0], u[SR - 2][1]);
-      xlast(xl0, xl1);
-      sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
-      sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
+      if (!fin) {
+        xlast(xl0, xl1);
+        sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
+        sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
+      }
       // (read only after the final band barrier; rewritten by the next region behind its iteration-0 barrier)
       if constexpr (FUSED_EPI) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
       save_x(2 + t - tstart);
