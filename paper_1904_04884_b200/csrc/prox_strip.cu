@@ -596,9 +596,11 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       const int b = t & 1;  // buffers holding this iteration's band-top rp / band-bottom X
       // single pass (T <= 8): the momentum schedule from the parameter bank
       const float2 bt2 = splat2(PH == 0 ? a.fgpb[t] : __ldg(a.fgp_beta + t));
-      // final step of a single pass: the epilogue reads only p, q, so the
-      // extrapolated duals, the band's X and its band-top rp are not formed
-      const bool fin = PH == 0 && t == tend - 1;
+      // final step of a single pass or of a multi-pass FGP's last pass: the
+      // epilogue reads only p, q, so the extrapolated duals, the band's X and
+      // its band-top rp are not formed (the walk's saved X of that step is
+      // never fetched: the epilogue exchanges through its own slots)
+      const bool fin = (PH == 0 || PH == 3) && t == tend - 1;
       // one row's dual update from its u, given the u of the row above
       auto update = [&](int s, float2 u0, float2 u1, float2 up0, float2 up1) {
         float2 gx0, gx1;
