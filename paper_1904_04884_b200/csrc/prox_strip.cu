@@ -574,7 +574,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       xlast(xl0, xl1);
       sm.top[lastbuf][w][lane] = f4(rp[0][0], rp[0][1]);
       sm.bot[lastbuf][w + 1][lane] = f4(xl0, xl1);
-      if constexpr (FUSED_EPI) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
+      if constexpr (FUSED_EPI)  // (T = 1: iteration 0 is the final step)
+        if ((TT > 0 ? TT : a.t1) == 1) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
       save_x(1);
       band_arrive(&bbar[lastbuf]);
       fetch_above(lastbuf, 1);  // read by band 0 itself only: after its arrival
@@ -651,8 +652,10 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         sm.top[b ^ 1][w][lane] = f4(rp[0][0], rp[0][1]);  // other buffers: slower warps may still read b
         sm.bot[b ^ 1][w + 1][lane] = f4(xl0, xl1);
       }
-      // (read only after the final band barrier; rewritten by the next region behind its iteration-0 barrier)
-      if constexpr (FUSED_EPI) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
+      // (read only after the final band barrier, so only the final step's matters;
+      // rewritten by the next region behind its iteration-0 barrier)
+      if constexpr (FUSED_EPI)
+        if (fin) ptop[w * 32 + lane] = f4(p[0][0], p[0][1]);
       save_x(2 + t - tstart);
       band_arrive(&bbar[b ^ 1]);
       fetch_above(b ^ 1, 2 + t - tstart);

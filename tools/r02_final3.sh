@@ -1,11 +1,10 @@
-# Round-2 closing measurements after the radix-32 adjoint columns
-mkdir -p gpurun_out/r02h
-timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r02h/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/r02h/pytest_gpu.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02h/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r02h/smoke.log
-timeout 1500 python bench.py --steps 20 --warmup 5 > gpurun_out/r02h/bench_c3.json 2> gpurun_out/r02h/bench_c3.err
-timeout 900 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02h/bench_c2.json 2> gpurun_out/r02h/bench_c2.err
-timeout 900 python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02h/bench_c5.json 2> gpurun_out/r02h/bench_c5.err
-timeout 1200 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02h/bench_c4.json 2> gpurun_out/r02h/bench_c4.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r02h/launches.csv python bench.py --steps 1 --warmup 3 --iters 10 --no-cpu-baseline --no-e2e > gpurun_out/r02h/launches.log 2>&1
+# Round-2 closing measurements after the final-step dead-work removal
+mkdir -p gpurun_out/r02i
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r02i/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/r02i/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02i/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r02i/smoke.log
+timeout 1500 python bench.py --steps 20 --warmup 5 > gpurun_out/r02i/bench_c3.json 2> gpurun_out/r02i/bench_c3.err
+timeout 900 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02i/bench_c2.json 2> gpurun_out/r02i/bench_c2.err
+timeout 900 python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02i/bench_c5.json 2> gpurun_out/r02i/bench_c5.err
+timeout 1200 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02i/bench_c4.json 2> gpurun_out/r02i/bench_c4.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r02i/launches.csv python bench.py --steps 1 --warmup 3 --iters 10 --no-cpu-baseline --no-e2e > gpurun_out/r02i/launches.log 2>&1
 echo done
-timeout 1500 ncu --set full --import-source on --clock-control none -k regex:"k_adj_cols|k_prox_strip" -s 16 -c 2 -o gpurun_out/r02h/adjprox python bench.py --steps 1 --warmup 1 --iters 10 --no-cpu-baseline --no-e2e > gpurun_out/r02h/adjprox.log 2>&1
