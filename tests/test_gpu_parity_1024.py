@@ -8,7 +8,9 @@ own sampled configuration) and 2048^2 x 4 planes.
 * C5 weights: lambda = (0.05, 1.0), T = 20 -> the multi-pass strip walk
   (7 + 7 + 6 FGP steps) with saved rows at production width;
 * C4's plane size with C3's weights: 2048-point rows (radix-64 + 32) and
-  columns (16 x 16 x 8), 40 x 40 prox regions per plane.
+  columns (16 x 16 x 8), 40 x 40 prox regions per plane;
+* 512 x 512 x 8 with C3's weights: the radix-32 adjoint columns at 16
+  threads per line.
 
 Bar (north_star): identical iterations / restarts / accepted step, history
 within 2e-5, volume rel-L2 <= 1e-4, identical detected-particle counts
@@ -30,6 +32,8 @@ CASES = {
     "c3": (1024, 16, 1500, False, 2, 0.5, 0.2, 5, 5),
     "c5": (1024, 16, 120, True, 4, 0.05, 1.0, 20, 3),
     "c4": (2048, 4, 2000, False, 3, 0.5, 0.2, 5, 3),
+    # 512-point columns and rows (radix-32 adjoint columns, 16-thread lines)
+    "c512": (512, 8, 600, False, 5, 0.5, 0.2, 5, 4),
 }
 
 
