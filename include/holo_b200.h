@@ -65,6 +65,9 @@ typedef struct {
   int32_t attempts; /* prox-gradient attempts incl. backtracking and restarts */
   double step_size, final_sparsity, wall_time, f0;
   int64_t nnz;
+  /* all-zero planes the forward passes skipped (solver.py:115-119), summed
+   * over attempts and ranks (the guard fix-up's redone forward not counted) */
+  int64_t skipped_planes;
 } holo_report;
 
 const char* holo_last_error(void);

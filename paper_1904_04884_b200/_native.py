@@ -43,7 +43,8 @@ class Report(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("restarts", ctypes.c_int32), ("diverged", ctypes.c_int32),
                 ("guard_fixups", ctypes.c_int32), ("attempts", ctypes.c_int32),
                 ("step_size", ctypes.c_double), ("final_sparsity", ctypes.c_double),
-                ("wall_time", ctypes.c_double), ("f0", ctypes.c_double), ("nnz", ctypes.c_int64)]
+                ("wall_time", ctypes.c_double), ("f0", ctypes.c_double), ("nnz", ctypes.c_int64),
+                ("skipped_planes", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p

@@ -32,6 +32,7 @@
 
 #include "../../include/holo_b200.h"
 #include "kernels.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace holo {
 
@@ -131,6 +132,9 @@ struct Prof {
     for (int i = 0; i < PK_N; ++i) { ms[i] = 0; cnt[i] = 0; }
   }
   cudaError_t begin(int k, cudaStream_t s) {
+    // NVTX range per kernel class (header-only NVTX3: a no-op unless a tool
+    // such as nsys / ncu --nvtx is attached)
+    nvtxRangePushA(kProfNames[k]);
     cur = on && ((mask >> k) & 1u);
     if (!cur) return cudaSuccess;
     if ((int)kind.size() <= used) {
@@ -146,6 +150,7 @@ struct Prof {
     return cudaEventRecord(ev[2 * used], s);
   }
   cudaError_t end(cudaStream_t s) {
+    nvtxRangePop();
     if (!cur) return cudaSuccess;
     cur = false;
     cudaError_t e = cudaEventRecord(ev[2 * used + 1], s);
@@ -270,7 +275,7 @@ struct LocalGroup {
 };
 
 // host scalar block (pinned) layout
-enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_FY, SC_FNEW, SC_F0, SC_AUX, SC_N };
+enum Slot { SC_IP = 0, SC_DX2, SC_L1, SC_TV, SC_FAIL, SC_DEAD, SC_FY, SC_FNEW, SC_F0, SC_AUX, SC_N };
 
 struct Engine {
   holo_geometry geom{};
@@ -363,6 +368,11 @@ struct Engine {
   double* plane_out = nullptr;  // [nzl][4]
   int* new_fail = nullptr;      // [nzl]
   uint8_t* force_acc = nullptr; // [nzl]
+  // sparsity-aware forward (solver.py:115-119): live[k] = 0 marks a stack
+  // plane of the newest prox output that is all zero, so the forward row and
+  // column passes skip it (HOLO_NO_PLANE_SKIP=1 turns the skipping off)
+  uint8_t* live = nullptr;      // [nzl]
+  bool plane_skip = std::getenv("HOLO_NO_PLANE_SKIP") == nullptr;
   float* fgp_beta = nullptr;
   int fgp_cap = 0;
   int fgp_inner = -1;  // depth whose momentum schedule fgp_beta holds
@@ -400,7 +410,7 @@ struct Engine {
     for (auto& p : S) cudaFree(p);
     cudaFree(scratch); cudaFree(Spart); cudaFree(Bspec); cudaFree(R); cudaFree(b64);
     cudaFree(sens_part); cudaFree(scal); cudaFreeHost(h_scal); cudaFree(prox_part);
-    cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(fgp_beta);
+    cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(live); cudaFree(fgp_beta);
     cudaFree(coo_counts); cudaFree(coo_offsets);
     cudaFree(coo_rows); cudaFree(coo_cols); cudaFree(coo_vals);
     for (int i = 0; i < 2; ++i) {
@@ -475,6 +485,7 @@ struct Engine {
     HOLO_CUDA(dalloc(plane_out, (size_t)std::max(nzl, 1) * 4));
     HOLO_CUDA(dalloc(new_fail, std::max(nzl, 1)));
     HOLO_CUDA(dalloc(force_acc, std::max(nzl, 1)));
+    HOLO_CUDA(dalloc(live, std::max(nzl, 1)));
     return ensure_scratch();
   }
 
@@ -568,10 +579,11 @@ struct Engine {
   }
 
   // S_out = A x (spectrum, band mask not applied; allreduced over ranks)
-  int forward_spectrum(const float2* x, float2* S_out, cudaStream_t s) {
+  // skip (optional): per-plane live flags of x from prox_reduce
+  int forward_spectrum(const float2* x, float2* S_out, cudaStream_t s, const uint8_t* skip = nullptr) {
     const int g = std::min(groups, fwd_groups(plan, std::max(nzs, 1)));  // (Spart holds `groups` partials)
-    PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzs * geom.ny, false, 1.0f, s));
-    PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzs, kb, g, s, packed));
+    PROF(PK_FWD_ROWS, s, fft_rows(plan, x, scratch, (long long)nzs * geom.ny, false, 1.0f, s, skip, geom.ny));
+    PROF(PK_FWD_COLS, s, fwd_cols(plan, scratch, Spart, nzs, kb, g, s, packed, skip));
     if (peer_on && nranks > 1) {  // fused group sum + reduce-scatter + all-gather over peer memory
       HOLO_CUDA(prof.begin(PK_SUM_GROUPS, s));
       int rc = peer_reduce(S_out, g, s);
@@ -625,10 +637,15 @@ struct Engine {
   int prox_step(ProxArgs& a, cudaStream_t s) {
     PROF(PK_PROX, s, prox(a, s));
     HOLO_CUDA(prof.begin(PK_REDUCE, s));
-    HOLO_CUDA(prox_reduce(a, a.tau_tv, a.tau_tv > 0.f, force_acc, plane_out, new_fail, s));
-    HOLO_CUDA(plane_total(plane_out, new_fail, nzs, scal, s));
+    // sum |x_new| == 0 proves an all-zero plane when no nonzero pixel can add
+    // an underflowed 0: real mode sums x itself; the complex soft threshold's
+    // |x| term is >= 2^-24 tau_l1 for every surviving pixel, normal for
+    // tau_l1 >= 1e-15 (prox_strip.cu epilogue, k_prox hypot in fp64)
+    const int skip_ok = a.real_mode || a.tau_l1 >= 1e-15f;
+    HOLO_CUDA(prox_reduce(a, a.tau_tv, a.tau_tv > 0.f, force_acc, plane_out, new_fail, s, live, skip_ok));
+    HOLO_CUDA(plane_total(plane_out, new_fail, nzs, scal, s, live));
     HOLO_CUDA(prof.end(s));
-    return allreduce_scalars(scal, SC_FAIL + 1, s);
+    return allreduce_scalars(scal, SC_DEAD + 1, s);
   }
 
   int real_opnorm_value(double& out, cudaStream_t s) {
@@ -722,7 +739,7 @@ struct Engine {
       // and its data term, queued behind the prox without a host round trip:
       // the guard flag is read back together with f_new
       auto forward_fnew = [&]() -> int {
-        int r2 = forward_spectrum(X[c], S[c], s);
+        int r2 = forward_spectrum(X[c], S[c], s, plane_skip ? live : nullptr);
         if (r2) return r2;
         HOLO_CUDA(prof.begin(PK_SENSOR, s));
         HOLO_CUDA(sensor(plan, S[c], nullptr, 1.f, 0.f, Bspec, nullptr, sens_part, s));
@@ -731,6 +748,7 @@ struct Engine {
         return read_scalars(s);
       };
       if ((rc = forward_fnew())) return rc;
+      if (plane_skip) last.skipped_planes += (long long)(h_scal[SC_DEAD] + 0.5);
       if (h_scal[SC_FAIL] > 0.5) {
         // guard fix-up: planes whose TV output was worse than its input take the
         // identity for that part (prox.py:138-147); rare, so the speculative
@@ -818,6 +836,10 @@ struct Engine {
 
   // solver.py:254-379
   int solve(const double* b_dev, const holo_solver_config& cfg, holo_report& rep, cudaStream_t s) {
+    nvtxRangePushA("holo_solve");
+    struct PopOnExit {
+      ~PopOnExit() { nvtxRangePop(); }
+    } pop_on_exit;
     auto t0 = std::chrono::steady_clock::now();
     int rc;
     if (cfg.max_iters < 1) return fail(HOLO_ERR_INVALID, "max_iters must be >= 1");

@@ -146,7 +146,8 @@ constexpr int row_tw_f2() {
 #endif
 template <int N, bool INV, int E_>
 __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __restrict__ in, float2* __restrict__ out,
-                                                          long long nrows, float scale, const float4* __restrict__ twg) {
+                                                          long long nrows, float scale, const float4* __restrict__ twg,
+                                                          const uint8_t* __restrict__ live, int rpp) {
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int RPC = row_threads<E_>() / TPF;
@@ -158,7 +159,11 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
   const int lr = threadIdx.x / TPF, j = threadIdx.x % TPF;
   for (long long row0 = (long long)blockIdx.x * RPC; row0 < nrows; row0 += (long long)gridDim.x * RPC) {
     const long long row = row0 + lr;
-    const bool active = row < nrows;
+    bool active = row < nrows;
+    if (live) {  // sparsity-aware forward (solver.py:115-119): rows of all-zero planes are skipped
+      if (active && !live[(int)row / rpp]) active = false;
+      if (!__syncthreads_or(active)) continue;  // the whole row group: no FFT either
+    }
     float2 v[E];
     const float2* src = in + row * N + j;
 #pragma unroll
@@ -169,8 +174,8 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
     // 14.48 -> 12.83 ms per 10 iterations, C4's 2048-point rows 26.4 -> 20.4)
     if (threadIdx.x == 0) {
       const long long nr0 = row0 + (long long)HOLO_ROW_PF_DIST * gridDim.x * RPC;
-      if (nr0 < nrows) {
-        const long long cnt = nrows - nr0 < RPC ? nrows - nr0 : RPC;
+      const long long cnt = nrows - nr0 < RPC ? nrows - nr0 : RPC;
+      if (nr0 < nrows && (!live || live[(int)nr0 / rpp] || live[(int)(nr0 + cnt - 1) / rpp])) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(in + nr0 * N),
                      "r"((unsigned)(cnt * N * sizeof(float2)))
                      : "memory");
@@ -353,6 +358,19 @@ HD float2 fwd_close(float2 acc, float2 accb, uint64_t t, int k0, int kb, const f
   }
 }
 
+// Horner step of an all-zero plane: acc <- acc z (+ 0), the same values as
+// the full step with v = 0 (fma(a, b, 0) = a b), without loading the plane
+template <bool PK, int E>
+__device__ __forceinline__ void horner_zero(float2 (&acc)[E], float2 (&accb)[PK ? E : 1], const float (&zx)[E],
+                                            const float2 (&zyy)[E]) {
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    acc[m] = fma2(swp(acc[m]), zyy[m], mul2(acc[m], splat2(zx[m])));
+    if constexpr (PK)
+      accb[m] = fma2(swp(accb[m]), make_float2(-zyy[m].x, -zyy[m].y), mul2(accb[m], splat2(zx[m])));
+  }
+}
+
 // K5: Spart[g] = sum over planes k of group g of column-FFT(in[k]) * conj(H_{k0+k})
 template <int N, int C, int E_, bool PK = false>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const float2* __restrict__ in,
@@ -360,7 +378,8 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
                                                                     int nzl, int ppg, int k0,
                                                                     const uint64_t* __restrict__ tab,
                                                                     const float4* __restrict__ twg,
-                                                                    const float2* __restrict__ circg) {
+                                                                    const float2* __restrict__ circg,
+                                                                    const uint8_t* __restrict__ live) {
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   extern __shared__ float2 smem[];
@@ -385,6 +404,10 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF) k_fwd_cols(const flo
 #pragma unroll
   for (int m = 0; m < E; ++m) fwd_ratio<PK>(tab[p0 + m * st], circ, zx[m], zyy[m]);
   for (int k = ke - 1; k >= kb; --k) {
+    if (live && !live[k]) {  // all-zero plane: v = 0
+      horner_zero<PK, E>(acc, accb, zx, zyy);
+      continue;
+    }
     float2 v[E];
     const float2* src = in + (long long)k * P + p0;
 #pragma unroll
@@ -419,7 +442,7 @@ template <int N, int C, int E_, bool PK = false>
 __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftShape<N, E_>::TPF <= 128 ? HOLO_FWD_MINB : 1)) k_fwd_cols_staged(
     const __grid_constant__ CUtensorMap in_map, float2* __restrict__ Spart, int nx, long long P, int ny, int nzl,
     int ppg, int k0, const uint64_t* __restrict__ tab, const float4* __restrict__ twg,
-    const float2* __restrict__ circg) {
+    const float2* __restrict__ circg, const uint8_t* __restrict__ live) {
   using Sh = FftShape<N, E_>;
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int BOX_ROWS = N < 256 ? N : 256;
@@ -452,7 +475,17 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftSha
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (leader && kb < ke) issue(ke - 1, 0);  // planes are walked last to first (Horner)
+  // sparsity-aware forward (solver.py:115-119): all-zero planes (live[k] == 0)
+  // are neither loaded nor transformed; the stage ring advances per live plane
+  auto next_live = [&](int k) {
+    if (live)
+      while (k >= kb && !live[k]) --k;
+    return k;
+  };
+  {
+    const int kf = next_live(ke - 1);
+    if (leader && kf >= kb) issue(kf, 0);  // planes are walked last to first (Horner)
+  }
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
@@ -473,10 +506,18 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftSha
   float2 zyy[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) fwd_ratio<PK>(tab[p0 + m * st], circ, zx[m], zyy[m]);
+  int i = 0;  // live planes consumed so far
   for (int k = ke - 1; k >= kb; --k) {
-    const int i = ke - 1 - k, b = i & 1;
-    // the other stage was last read in the previous plane, before fft_line's barriers
-    if (leader && k - 1 >= kb) issue(k - 1, b ^ 1);
+    if (live && !live[k]) {  // v = 0
+      horner_zero<PK, E>(acc, accb, zx, zyy);
+      continue;
+    }
+    const int b = i & 1;
+    // the other stage was last read in the previous live plane, before fft_line's barriers
+    if (leader) {
+      const int kn = next_live(k - 1);
+      if (kn >= kb) issue(kn, b ^ 1);
+    }
     {
       const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]), par = (i >> 1) & 1;
       unsigned done = 0;
@@ -499,6 +540,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftSha
       if constexpr (PK)
         accb[m] = fma2(swp(accb[m]), make_float2(-zyy[m].x, -zyy[m].y), fma2(accb[m], splat2(zx[m]), v[m]));
     }
+    ++i;
   }
   // times conj(H_kb) (packed: the two-sum closure), exact (64-bit phase)
 #pragma unroll
@@ -791,7 +833,8 @@ constexpr int kReduceThreads = 128;
 __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __restrict__ part, int tpp, int nw,
                                                                 double tau, int tv_on, uint8_t* __restrict__ force_acc,
                                                                 double* __restrict__ plane_out,
-                                                                int* __restrict__ new_fail) {
+                                                                int* __restrict__ new_fail,
+                                                                uint8_t* __restrict__ live, int skip_ok) {
   const int plane = blockIdx.x;
   double acc[kProxParts];
 #pragma unroll
@@ -832,19 +875,23 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
     o[1] = s[PT_DX2];
     o[2] = s[PT_L1];
     o[3] = s[PT_TVX];
+    // all-zero plane: sum |x_new| == 0 exactly (NaN compares unequal: live)
+    if (live) live[plane] = (skip_ok && s[PT_L1] == 0.0) ? 0 : 1;
   }
 }
 
 __global__ void __launch_bounds__(kReduceThreads) k_plane_total(const double* __restrict__ plane_out,
                                                                 const int* __restrict__ new_fail, int nplanes,
-                                                                double* __restrict__ scalars) {
-  double acc[5] = {0, 0, 0, 0, 0};
+                                                                double* __restrict__ scalars,
+                                                                const uint8_t* __restrict__ live) {
+  double acc[6] = {0, 0, 0, 0, 0, 0};
   for (int k = threadIdx.x; k < nplanes; k += kReduceThreads) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] += plane_out[(long long)k * 4 + i];
     acc[4] += (double)new_fail[k];
+    if (live) acc[5] += live[k] ? 0.0 : 1.0;
   }
-  block_sum<5, kReduceThreads>(acc, scalars);
+  block_sum<6, kReduceThreads>(acc, scalars);
 }
 
 // ------------------------------------------------------------ misc ---------
@@ -1095,7 +1142,8 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
 }
 
 cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
-                     cudaStream_t s) {
+                     cudaStream_t s, const uint8_t* live, int rows_per_plane) {
+  if (live && (rows_per_plane <= 0 || nrows >= (1LL << 31))) return cudaErrorInvalidValue;
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.nx, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1107,11 +1155,13 @@ cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nro
     const int grid = grid_for((nrows + RPC - 1) / RPC, 1, 148 * 64);
     if (inverse) {
       err = set_smem(k_fft_rows<N, true, E>, smem);
-      k_fft_rows<N, true, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
+      k_fft_rows<N, true, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()], live,
+                                                                  rows_per_plane);
   COUNT_LAUNCH(1);
     } else {
       err = set_smem(k_fft_rows<N, false, E>, smem);
-      k_fft_rows<N, false, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()]);
+      k_fft_rows<N, false, E><<<grid, NT, smem, s>>>(in, out, nrows, scale, p.tw_x[tw_slot<E>()], live,
+                                                                  rows_per_plane);
   COUNT_LAUNCH(1);
     }
   });
@@ -1244,7 +1294,7 @@ int fwd_groups(const Plan& p, int nzl) {
 }
 
 cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
-                     bool packed) {
+                     bool packed, const uint8_t* live) {
   cudaError_t err = cudaSuccess;
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
@@ -1263,7 +1313,7 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
       auto go = [&](auto kern) {
         if ((err = set_smem(kern, smem))) return;
         kern<<<grid, NT, smem, s>>>(map, Spart, p.nx, p.P, p.ny, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()],
-                                    p.circle);
+                                    p.circle, live);
       };
       if (packed)
         go(k_fwd_cols_staged<N, C, E, true>);
@@ -1273,7 +1323,8 @@ cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, in
       const size_t smem = col_smem<N, C, E>(256);
       auto go = [&](auto kern) {
         if ((err = set_smem(kern, smem))) return;
-        kern<<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle);
+        kern<<<grid, NT, smem, s>>>(in, Spart, p.nx, p.P, nzl, ppg, k0, p.phase, p.tw_y[tw_slot<E>()], p.circle,
+                                    live);
       };
       if (packed)
         go(k_fwd_cols<N, C, E, true>);
@@ -1369,15 +1420,16 @@ cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
 }
 
 cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
-                        int* new_fail, cudaStream_t s) {
+                        int* new_fail, cudaStream_t s, uint8_t* live, int skip_ok) {
   k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, a.kind == 1 ? a.part_warps : 0,
-                                                     tau_tv, tv_on, force_acc, plane_out, new_fail);
+                                                     tau_tv, tv_on, force_acc, plane_out, new_fail, live, skip_ok);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }
 
-cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplanes, double* scalars, cudaStream_t s) {
-  k_plane_total<<<1, kReduceThreads, 0, s>>>(plane_out, new_fail, nplanes, scalars);
+cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplanes, double* scalars, cudaStream_t s,
+                        const uint8_t* live) {
+  k_plane_total<<<1, kReduceThreads, 0, s>>>(plane_out, new_fail, nplanes, scalars, live);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

@@ -90,16 +90,19 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
 void plan_free(Plan& p);
 
 // batched 1D transforms (unnormalised; `scale` multiplies the output)
+// live (optional, forward rows): live[row / rows_per_plane] == 0 marks an
+// all-zero plane whose rows are neither read, transformed nor written
 cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
-                     cudaStream_t s);
+                     cudaStream_t s, const uint8_t* live = nullptr, int rows_per_plane = 0);
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
                      cudaStream_t s);
 // adjoint column pass: out[k] = colIFFT(H_{k0+k} * R), k < nzl (R already band-masked)
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s,
                      bool packed = false);  // packed: the packed real engine's stack (engine.cu)
-// forward column pass: Spart[g] = sum_{k in group g} colFFT(in[k]) * conj(H_{k0+k})
+// forward column pass: Spart[g] = sum_{k in group g} colFFT(in[k]) * conj(H_{k0+k});
+// planes with live[k] == 0 (optional) are all zero and skipped (solver.py:115-119)
 cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
-                     bool packed = false);
+                     bool packed = false, const uint8_t* live = nullptr);
 int fwd_groups(const Plan& p, int nzl);
 cudaError_t sum_groups(const Plan& p, const float2* Spart, int groups, float2* S, cudaStream_t s);
 
@@ -123,12 +126,16 @@ cudaError_t prox_strip(const ProxArgs& a, cudaStream_t s);
 cudaError_t prox(const ProxArgs& a, cudaStream_t s);
 // per-plane reduction of the prox partials + guard check.  force_acc[plane]
 // accumulates the guard bits; plane_out[plane*4 + {0..3}] = ip, dx2, l1, tv;
-// new_fail[plane] = 1 when a guard bit was newly raised.
+// new_fail[plane] = 1 when a guard bit was newly raised.  live (optional):
+// live[plane] = 0 when skip_ok and the plane's sum |x_new| is exactly 0, i.e.
+// every x_new of the plane is zero (the caller sets skip_ok only where a
+// nonzero pixel cannot contribute an underflowed 0 to that sum).
 cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
-                        int* new_fail, cudaStream_t s);
-// scalars[0..3] += sums of plane_out over planes (fixed order); scalars[4] = #new guard failures
+                        int* new_fail, cudaStream_t s, uint8_t* live = nullptr, int skip_ok = 0);
+// scalars[0..3] += sums of plane_out over planes (fixed order); scalars[4] = #new guard failures;
+// scalars[5] = #planes with live == 0 (0 without live)
 cudaError_t plane_total(const double* plane_out, const int* new_fail, int nplanes, double* scalars,
-                        cudaStream_t s);
+                        cudaStream_t s, const uint8_t* live = nullptr);
 
 // b (fp64, host layout) -> fp32 complex plane (imag 0), per-block sum b^2
 cudaError_t load_hologram(const double* b, float2* bc, long long P, double* part, int* nblocks, cudaStream_t s);
