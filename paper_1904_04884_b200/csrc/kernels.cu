@@ -834,8 +834,15 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
                                                                 double tau, int tv_on, uint8_t* __restrict__ force_acc,
                                                                 double* __restrict__ plane_out,
                                                                 int* __restrict__ new_fail,
-                                                                uint8_t* __restrict__ live, int skip_ok) {
+                                                                uint8_t* __restrict__ live, int skip_ok,
+                                                                const uint8_t* __restrict__ only) {
   const int plane = blockIdx.x;
+  // guard fix-up pass (only = its force bits): planes it did not rerun keep
+  // the main pass's sums
+  if (only && !only[plane]) {
+    if (threadIdx.x == 0) new_fail[plane] = 0;
+    return;
+  }
   double acc[kProxParts];
 #pragma unroll
   for (int i = 0; i < kProxParts; ++i) acc[i] = 0.0;
@@ -1422,7 +1429,8 @@ cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
 cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* force_acc, double* plane_out,
                         int* new_fail, cudaStream_t s, uint8_t* live, int skip_ok) {
   k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, a.kind == 1 ? a.part_warps : 0,
-                                                     tau_tv, tv_on, force_acc, plane_out, new_fail, live, skip_ok);
+                                                     tau_tv, tv_on, force_acc, plane_out, new_fail, live, skip_ok,
+                                                     a.force);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }
