@@ -7,7 +7,20 @@ HDR := $(wildcard paper_1904_04884_b200/csrc/*.cuh) include/holo_b200.h
 LIB := paper_1904_04884_b200/libholo_b200.so
 OBJ := $(patsubst paper_1904_04884_b200/csrc/%.cu,build/%.o,$(SRC))
 
+CLIB := paper_1904_04884_b200/libholo_b200_checked.so
+COBJ := $(patsubst paper_1904_04884_b200/csrc/%.cu,build/checked/%.o,$(SRC))
+
 all: $(LIB)
+
+# bounds-checked build (HOLO_CHECKS, common.cuh): tests/test_gpu_checked.py
+checked: $(CLIB)
+
+build/checked/%.o: paper_1904_04884_b200/csrc/%.cu $(HDR)
+	@mkdir -p build/checked
+	$(NVCC) $(NVFLAGS) -DHOLO_CHECKS -c $< -o $@
+
+$(CLIB): $(COBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(COBJ) -ldl
 
 build/%.o: paper_1904_04884_b200/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -17,6 +30,6 @@ $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) -ldl
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CLIB)
 
-.PHONY: all clean
+.PHONY: all checked clean

@@ -72,6 +72,12 @@ typedef struct {
 
 const char* holo_last_error(void);
 int holo_version(void);
+/* Checked build only (make checked -> libholo_b200_checked.so): *bits = the
+ * bounds-check violations the kernels recorded since the last call (common.cuh
+ * HoloCheckBit; read and cleared after a device sync).  Returns 1 in the
+ * checked build, 0 (and *bits = 0) in the normal one.  No reference
+ * counterpart: compute-sanitizer substitute for test infrastructure. */
+int holo_debug_checks(uint32_t* bits);
 /* 1 if this build handles the plane shape (FFT sizes: powers of two 8..4096) */
 int holo_shape_supported(int32_t nx, int32_t ny);
 

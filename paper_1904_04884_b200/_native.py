@@ -14,6 +14,10 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libholo_b200.so")
+# HOLO_LIB_PATH: another build of the same ABI, e.g. the bounds-checked
+# libholo_b200_checked.so (make checked) for tests/test_gpu_checked.py
+LIB_PATH = os.environ.get("HOLO_LIB_PATH", LIB_PATH)
+CHECKED_LIB_PATH = os.path.join(_HERE, "libholo_b200_checked.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "holo_b200.h")
 
 HOLO_OK = 0
@@ -56,6 +60,7 @@ _H = ctypes.c_void_p  # holo_handle*
 SIGNATURES = {
     "holo_last_error": (ctypes.c_char_p, []),
     "holo_version": (ctypes.c_int, []),
+    "holo_debug_checks": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
     "holo_shape_supported": (ctypes.c_int, [_I, _I]),
     "holo_create": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.POINTER(_H)]),
     "holo_nccl_unique_id": (ctypes.c_int, [_P]),

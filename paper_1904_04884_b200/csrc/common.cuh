@@ -6,7 +6,60 @@
 
 #define HD __device__ __forceinline__
 
+// Checked build (make checked -> libholo_b200_checked.so, -DHOLO_CHECKS): the
+// kernels test their global indices, tensor-copy boxes and region frames
+// against the buffers' bounds and record violations as bits in a per-file
+// device word (no trap: the run completes and holo_debug_checks reports);
+// the prox poisons its shared memory with NaN before use and the engine fills
+// fresh device buffers with 0xFF (NaN), so a value read from a never-written
+// slot or allocation reaches the output as NaN.  compute-sanitizer is closed
+// on the GPU pool this was built on; this is the substitute.  The normal build
+// compiles all of it away.
+enum HoloCheckBit : unsigned {
+  CK_PROX_FRAME = 1u << 0,   // a strip-prox region frame outside its plane
+  CK_PROX_STORE = 1u << 1,   // x_new / partial / multi-pass state index out of range
+  CK_ROWS = 1u << 2,         // row-pass index out of range
+  CK_COLS = 1u << 3,         // column-pass box / index out of range
+  CK_GENERIC = 1u << 4,      // generic prox index out of range
+  CK_COO = 1u << 5,          // COO compaction beyond its counted total
+  CK_SENSOR = 1u << 6,       // sensor / group-sum index out of range
+};
+#ifdef HOLO_CHECKS
+static __device__ unsigned int g_holo_check = 0u;
+#define HOLO_DCHECK(cond, bit)                                \
+  do {                                                        \
+    if (!(cond)) atomicOr(&::g_holo_check, (unsigned)(bit)); \
+  } while (0)
+// host side: read and clear this translation unit's word
+#define HOLO_CHECK_TU(fn)                                                              \
+  unsigned fn() {                                                                      \
+    unsigned v = 0, z = 0;                                                             \
+    cudaMemcpyFromSymbol(&v, ::g_holo_check, sizeof(v));                               \
+    cudaMemcpyToSymbol(::g_holo_check, &z, sizeof(z));                                 \
+    return v;                                                                          \
+  }
+#else
+#define HOLO_DCHECK(cond, bit) \
+  do {                         \
+  } while (0)
+#define HOLO_CHECK_TU(fn) \
+  unsigned fn() { return 0u; }
+#endif
+
 namespace holo {
+
+// checked build: fill this block's dynamic shared memory with NaN (then a
+// CTA barrier) so a read of a never-written slot shows up in the output
+HD void poison_dyn_smem() {
+#ifdef HOLO_CHECKS
+  extern __shared__ __align__(16) float4 holo_poison_smem[];
+  unsigned bytes;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(bytes));
+  const float nan = __int_as_float(0x7fffffff);
+  for (unsigned i = threadIdx.x; i < bytes / 16u; i += blockDim.x) holo_poison_smem[i] = make_float4(nan, nan, nan, nan);
+  __syncthreads();
+#endif
+}
 
 
 // Packed fp32x2 arithmetic (sm_100 FADD2/FMUL2/FFMA2): one instruction

@@ -110,7 +110,12 @@ static NcclApi& nccl() {
 template <class T>
 static cudaError_t dalloc(T*& p, size_t count) {
   if (p) return cudaSuccess;
-  return cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1));
+  cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1));
+#ifdef HOLO_CHECKS
+  // checked build: fresh buffers read as NaN / -1 until written
+  if (!e) e = cudaMemset(p, 0xFF, sizeof(T) * std::max<size_t>(count, 1));
+#endif
+  return e;
 }
 
 // Per-kernel-class device timing with CUDA events on the launching stream
@@ -977,6 +982,17 @@ extern "C" {
 
 const char* holo_last_error(void) { return holo::g_err.c_str(); }
 int holo_version(void) { return 1; }
+
+int holo_debug_checks(uint32_t* bits) {
+  cudaDeviceSynchronize();
+  const unsigned v = holo::check_bits_kernels() | holo::check_bits_prox();
+  if (bits) *bits = v;
+#ifdef HOLO_CHECKS
+  return 1;
+#else
+  return 0;
+#endif
+}
 int holo_shape_supported(int32_t nx, int32_t ny) { return holo::plan_supported(nx, ny) ? 1 : 0; }
 
 int holo_create(const holo_geometry* geom, int device, holo_handle** out) {

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
   constexpr int TPF = Sh::TPF, E = Sh::E;
   constexpr int RPC = row_threads<E_>() / TPF;
   extern __shared__ float2 smem[];
+  poison_dyn_smem();
   float4* tw = reinterpret_cast<float4*>(smem);
   float2* buf = smem + row_tw_f2<N, E_>();
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(row_threads<E_>()) k_fft_rows(const float2* __
     }
     fft_line<N, INV, E_>(v, j, buf + lr * Sh::PADN, 1, tw);
     if (active) {
+      HOLO_DCHECK(row >= 0 && row < nrows && (!live || (int)row / rpp < (int)((nrows + rpp - 1) / rpp)), CK_ROWS);
       float2* dst = out + row * N + j;
       const float2 sc = splat2(scale);
 #pragma unroll
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 1 : (C * FftSha
   // plane k's stage; else the exchange buffer doubles as the stage
   constexpr bool kSep = adj_separate_stage<N, C, E_>();
   float2* stage = kSep ? buf + (((N + N / E_) * C + 15) & ~15) : buf;  // 128-byte aligned for the bulk stores
+  poison_dyn_smem();
   for (int i = threadIdx.x; i < TwLayout<N, E_>::size(); i += blockDim.x) tw[i] = twg[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) circ[i] = circg[i];
   __syncthreads();
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 1 : (C * FftSha
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (leader) {
+      HOLO_DCHECK(k >= 0 && k < nzl && (blockIdx.x + 1) * C <= nx, CK_COLS);
 #pragma unroll
       for (int r0 = 0; r0 < N; r0 += BOX_ROWS)
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
@@ -454,7 +458,9 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftSha
   __shared__ uint64_t bars[2];
   const int kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
   const bool leader = threadIdx.x == 0;
+  poison_dyn_smem();
   auto issue = [&](int k, int b) {
+    HOLO_DCHECK(k >= 0 && k < nzl && (blockIdx.x + 1) * C <= nx, CK_COLS);
     const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[b]);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
@@ -546,6 +552,7 @@ __global__ void __launch_bounds__(C * FftShape<N, E_>::TPF, PK ? 2 : (C * FftSha
 #pragma unroll
   for (int m = 0; m < E; ++m) acc[m] = fwd_close<PK>(acc[m], accb[PK ? m : 0], tab[p0 + m * st], k0, kb, circ);
   float2* dst = Spart + (long long)blockIdx.y * P + p0;
+  HOLO_DCHECK(p0 + (long long)(E - 1) * st < P && col < nx, CK_COLS);
 #pragma unroll
   for (int m = 0; m < E; ++m) dst[m * st] = acc[m];
 }
@@ -1147,6 +1154,8 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   return cudaSuccess;
 }
+
+HOLO_CHECK_TU(check_bits_kernels)
 
 cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
                      cudaStream_t s, const uint8_t* live, int rows_per_plane) {

@@ -89,6 +89,11 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
                        cudaStream_t s);
 void plan_free(Plan& p);
 
+// checked build (HOLO_CHECKS): read-and-clear the violation bits of each
+// translation unit (HoloCheckBit, common.cuh); 0 in the normal build
+unsigned check_bits_kernels();
+unsigned check_bits_prox();
+
 // batched 1D transforms (unnormalised; `scale` multiplies the output)
 // live (optional, forward rows): live[row / rows_per_plane] == 0 marks an
 // all-zero plane whose rows are neither read, transformed nor written

@@ -345,6 +345,12 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
   const bool ipdx = !FAST && a.ipdx;
   const TileGeom& tg = wk.tg;
   const int i0 = tg.i0, i1 = tg.i1, j0 = tg.j0, j1 = tg.j1, ri0 = tg.ri0, rj0 = tg.rj0;
+  // the frame lies in its plane (the garbage-zone argument needs clamped
+  // regions) and holds its tile
+  HOLO_DCHECK(plane >= 0 && plane < a.nplanes && ri0 >= 0 && ri0 + RH <= a.ny && rj0 >= 0 && rj0 + RW <= a.nx &&
+                  (rj0 & 1) == 0 && i0 >= ri0 && i1 <= ri0 + RH && j0 >= rj0 && j1 <= rj0 + RW && i0 < i1 &&
+                  j0 < j1,
+              CK_PROX_FRAME);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool lane0 = lane == 0, lane31 = lane == 31;
   const int r0 = w * SR;
@@ -671,6 +677,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         // parity-split rows (even columns, then odd): a warp's store is 512
         // contiguous bytes instead of every other 16 bytes of 1 KB
         const long long gs = (pass & 1) * a.sstride + g - (gj >> 1);  // row start + gj / 2
+        HOLO_DCHECK(gs >= 0 && gs + (a.nx >> 1) < 2 * a.sstride && g + 1 < a.sstride, CK_PROX_STORE);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           a.sbuf[gs + k * (a.nx >> 1)] = f4(p[s][k], q[s][k]);
@@ -851,6 +858,8 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         acc[PT_IP] += ip.x + ip.y;
         acc[PT_DX2] += d2.x + d2.y;
       }
+      HOLO_DCHECK(!cInt || (g >= (long long)plane * a.P && g + 1 < (long long)(plane + 1) * a.P && gj + 1 < a.nx),
+                  CK_PROX_STORE);
       if (cInt) *reinterpret_cast<float4*>(a.xnew + g) = f4(p[s][0], p[s][1]);
     }
   }
@@ -887,6 +896,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     const int slot = (lane >> 2) & 7;
     // per-warp fp32 partials straight to HBM; k_prox_reduce sums them in fp64
     // (no cross-warp barrier at the end of the region)
+    HOLO_DCHECK(tile >= 0 && tile < a.tiles_per_plane, CK_PROX_STORE);
     if ((lane & 3) == 0 && slot < kProxParts)
       reinterpret_cast<float*>(a.part)[(((long long)plane * kProxParts + slot) * a.tiles_per_plane + tile) * NW + w] = x;
   }
@@ -936,6 +946,7 @@ __global__ void __launch_bounds__(NT, 1) k_prox_strip(const ProxArgs a, const __
   int work = WALK ? strip_from(blockIdx.x) : next_from(blockIdx.x);
   if (work < 0) return;
   const bool leader = threadIdx.x == 0;
+  poison_dyn_smem();  // (checked build: never-written band slots / halo reads are NaN)
   if (leader) {
     mbar_init(&bars[0], 1);  // slot 0 (and the later passes' state slot)
     mbar_init(&bars[1], 1);
@@ -1029,6 +1040,8 @@ CUresult encode_state_map(CUtensorMap* m, const void* base, int ny_total, int nx
 }
 
 }  // namespace
+
+HOLO_CHECK_TU(check_bits_prox)
 
 int prox_strip_max_halo() { return 14; }
 
