@@ -50,3 +50,30 @@ def test_struct_layouts_match_header():
     assert nat.SolverConfig.real_nonnegative.offset == 60 and ctypes.sizeof(nat.SolverConfig) == 64
     assert nat.Report.step_size.offset == 24
     assert nat.Report.nnz.offset == 56
+
+
+def _header_struct_fields(name):
+    """Field names of `typedef struct {...} name;` in include/holo_b200.h, in order."""
+    import os
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "holo_b200.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    m = re.search(r"typedef struct \{([^{}]*)\}\s*" + name + ";", hdr)
+    assert m, name
+    fields = []
+    for decl in m.group(1).split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        names = decl.split(None, 1)[1]
+        fields += [n.strip() for n in names.split(",")]
+    return fields
+
+
+@pytest.mark.parametrize("cname,pyname", [("holo_geometry", "Geometry"), ("holo_solver_config", "SolverConfig"),
+                                          ("holo_report", "Report")])
+def test_ctypes_structs_follow_the_header(cname, pyname):
+    # the Python mirror of each ABI struct has the header's fields in the header's order
+    py = [f[0] for f in getattr(nat, pyname)._fields_]
+    assert py == _header_struct_fields(cname)
