@@ -528,7 +528,8 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "solve": {"iterations": rep.iterations, "restarts": rep.restarts, "nnz": rep.nnz,
-                      "final_sparsity": rep.final_sparsity, "attempts": rep.attempts},
+                      "final_sparsity": rep.final_sparsity, "attempts": rep.attempts,
+                      "skipped_planes": rep.skipped_planes},
             "cpu_baseline": cpu,
             "parity": parity,
             "e2e": e2e,
