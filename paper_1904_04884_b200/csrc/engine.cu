@@ -373,6 +373,9 @@ struct Engine {
   double* plane_out = nullptr;  // [nzl][4]
   int* new_fail = nullptr;      // [nzl]
   uint8_t* force_acc = nullptr; // [nzl]
+  float4* tv_wside = nullptr;    // prox tvfix side rows [nzl][tiles][2][32]
+  float* tv_bpart = nullptr;     // prox tvfix partials [nzl][3][tiles]
+  size_t tvfix_cap = 0;          // tiles the two hold
   // sparsity-aware forward (solver.py:115-119): live[k] = 0 marks a stack
   // plane of the newest prox output that is all zero, so the forward row and
   // column passes skip it (HOLO_NO_PLANE_SKIP=1 turns the skipping off)
@@ -416,6 +419,7 @@ struct Engine {
     cudaFree(scratch); cudaFree(Spart); cudaFree(Bspec); cudaFree(R); cudaFree(b64);
     cudaFree(sens_part); cudaFree(scal); cudaFreeHost(h_scal); cudaFree(prox_part);
     cudaFree(plane_out); cudaFree(new_fail); cudaFree(force_acc); cudaFree(live); cudaFree(fgp_beta);
+    cudaFree(tv_wside); cudaFree(tv_bpart);
     cudaFree(coo_counts); cudaFree(coo_offsets);
     cudaFree(coo_rows); cudaFree(coo_cols); cudaFree(coo_vals);
     for (int i = 0; i < 2; ++i) {
@@ -507,6 +511,20 @@ struct Engine {
       prox_part_cap = need;
     }
     a.part = prox_part;
+    if (a.tvfix) {  // boundary-row statistics (k_prox_tvfix): w side rows + per-tile partials
+      const size_t tiles = (size_t)std::max(nplanes, 1) * a.tiles_per_plane;
+      if (tiles > tvfix_cap) {
+        cudaFree(tv_wside);
+        cudaFree(tv_bpart);
+        tv_wside = nullptr;
+        tv_bpart = nullptr;
+        HOLO_CUDA(dalloc(tv_wside, tiles * 64));
+        HOLO_CUDA(dalloc(tv_bpart, tiles * 3));
+        tvfix_cap = tiles;
+      }
+      a.wside = tv_wside;
+      a.bpart = tv_bpart;
+    }
     if (a.pass_len) {  // multi-pass FGP state
       const long long n = (long long)std::max(nplanes, 1) * ny * nx;
       const long long tiles = (long long)std::max(nplanes, 1) * a.tiles_per_plane;

@@ -837,12 +837,59 @@ constexpr int kReduceThreads = 128;
 
 // part: per tile fp64 sums (generic kernel, nw == 0) or per (tile, warp) fp32
 // sums (strip kernel, nw warps per tile), summed here in fp64
+// Boundary-row statistics of the strip prox with tvfix (kernels.cuh): for
+// every tile below the first tile row, the TV(w) (guard, per part) and
+// TV(x_new) terms of its first row, whose row above lies in the tile above
+// (prox.py:61-72 isotropic TV, backward differences, zero at the plane's left
+// edge).  w of a tile's first / last row comes from the prox's side buffer,
+// x_new from the output.  One CTA of 64 threads per tile, fp32 partials per
+// tile -> bpart[plane][3][tile] (k_prox_reduce adds them in fp64).
+__global__ void __launch_bounds__(64) k_prox_tvfix(const ProxArgs a) {
+  const int tile = blockIdx.x, plane = blockIdx.y;
+  const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+  float g_re = 0.f, g_im = 0.f, tvx = 0.f;
+  if (ty > 0) {
+    const int i0 = ty * a.tile_h, j0 = tx * a.tile, j1 = min(a.nx, j0 + a.tile);
+    auto rj0_of = [&](int t) { return min(max(t * a.tile - a.halo, 0), a.nx - 64); };
+    const int rj0 = rj0_of(tx), j = j0 + (int)threadIdx.x;
+    if (j < j1) {
+      const float2* X = a.xnew + (long long)plane * a.P;
+      const float2 xa = X[(long long)i0 * a.nx + j], xu = X[(long long)(i0 - 1) * a.nx + j];
+      const float2 xl = j > 0 ? X[(long long)i0 * a.nx + j - 1] : xa;
+      const float2* W = reinterpret_cast<const float2*>(a.wside);  // [plane][tile][2][64]
+      const long long base = (long long)plane * a.tiles_per_plane;
+      auto wrow = [&](int t, int which) { return W + ((base + t) * 2 + which) * 64; };
+      HOLO_DCHECK(j - rj0 >= 0 && j - rj0 < 64 && i0 - 1 >= 0 && i0 < a.ny, CK_PROX_STORE);
+      const float2 wa = wrow(tile, 0)[j - rj0], wu = wrow(tile - a.tiles_x, 1)[j - rj0];
+      float2 wl = wa;
+      if (j > 0) wl = j - 1 >= j0 ? wrow(tile, 0)[j - 1 - rj0] : wrow(tile - 1, 0)[j - 1 - rj0_of(tx - 1)];
+      auto nrm = [](float gy, float gx) { return sqrt_a(fmaf(gy, gy, gx * gx)); };
+      g_re = nrm(wa.x - wu.x, wa.x - wl.x);
+      g_im = nrm(wa.y - wu.y, wa.y - wl.y);
+      tvx = nrm(xa.x - xu.x, xa.x - xl.x) + nrm(xa.y - xu.y, xa.y - xl.y);
+    }
+  }
+  __shared__ float red[2][3];
+  float v3[3] = {a.tau_tv * g_re, a.tau_tv * g_im, tvx};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v3[i] += __shfl_down_sync(0xffffffffu, v3[i], o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = v3[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3)
+    a.bpart[((long long)plane * 3 + threadIdx.x) * a.tiles_per_plane + tile] =
+        red[0][threadIdx.x] + red[1][threadIdx.x];
+}
+
 __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __restrict__ part, int tpp, int nw,
                                                                 double tau, int tv_on, uint8_t* __restrict__ force_acc,
                                                                 double* __restrict__ plane_out,
                                                                 int* __restrict__ new_fail,
                                                                 uint8_t* __restrict__ live, int skip_ok,
-                                                                const uint8_t* __restrict__ only) {
+                                                                const uint8_t* __restrict__ only,
+                                                                const float* __restrict__ bpart) {
   const int plane = blockIdx.x;
   // guard fix-up pass (only = its force bits): planes it did not rerun keep
   // the main pass's sums
@@ -869,6 +916,14 @@ __global__ void __launch_bounds__(kReduceThreads) k_prox_reduce(const double* __
     for (int t = threadIdx.x; t < tpp; t += kReduceThreads) {
 #pragma unroll
       for (int i = 0; i < kProxParts; ++i) acc[i] += src[(long long)t * kProxParts + i];
+    }
+  }
+  if (bpart) {  // boundary-row TV terms (k_prox_tvfix)
+    const float* b = bpart + (long long)plane * 3 * tpp;
+    for (int t = threadIdx.x; t < tpp; t += kReduceThreads) {
+      acc[PT_G_R] += (double)b[t];
+      acc[PT_G_I] += (double)b[tpp + t];
+      acc[PT_TVX] += (double)b[2 * tpp + t];
     }
   }
   __shared__ double s[kProxParts];
@@ -1409,7 +1464,13 @@ cudaError_t prox(const ProxArgs& a, cudaStream_t s) {
   if (a.kind == 1) {
     if (!a.pass_len || !(a.tau_tv > 0.f)) {  // no TV: nothing to split into passes
       COUNT_LAUNCH(1);
-      return prox_strip(a, s);
+      cudaError_t e = prox_strip(a, s);
+      if (!e && prox_tvfix_launch(a)) {
+        k_prox_tvfix<<<dim3(a.tiles_per_plane, a.nplanes), 64, 0, s>>>(a);
+        COUNT_LAUNCH(1);
+        e = cudaGetLastError();
+      }
+      return e;
     }
     if (!a.vbuf || !a.sbuf || !a.rbuf || !a.tvv) return cudaErrorInvalidValue;
     // guard fix-up (force): the state of every pass is still in HBM, rerun the last
@@ -1439,7 +1500,7 @@ cudaError_t prox_reduce(const ProxArgs& a, double tau_tv, int tv_on, uint8_t* fo
                         int* new_fail, cudaStream_t s, uint8_t* live, int skip_ok) {
   k_prox_reduce<<<a.nplanes, kReduceThreads, 0, s>>>(a.part, a.tiles_per_plane, a.kind == 1 ? a.part_warps : 0,
                                                      tau_tv, tv_on, force_acc, plane_out, new_fail, live, skip_ok,
-                                                     a.force);
+                                                     a.force, prox_tvfix_launch(a) ? a.bpart : nullptr);
   COUNT_LAUNCH(1);
   return cudaGetLastError();
 }

@@ -63,7 +63,20 @@ struct ProxArgs {
   // regions touch no plane edge); ordered launches visit those first
   int ix0 = 0, ix1 = 0, iy0 = 0, iy1 = 0, icnt = 0;
   float rcp_icnt = 0.f, rcp_ecnt = 0.f, rcp_nix = 0.f, rcp_ew = 0.f;
+  // strip kernel, single pass: top halo rows (halo_y) and the boundary-row
+  // statistics.  tvfix: the top halo is T instead of T + 1, so a tile's first
+  // row has no valid row above it in its own region; its TV(w) / TV(x_new)
+  // terms are left out there and added by k_prox_tvfix from wside (every
+  // tile's first and last rows of w) and x_new, into bpart [plane][3][tile]
+  int halo_y = 0, tvfix = 0;
+  float4* wside = nullptr;  // [nplanes][tiles_per_plane][2][32] float4 (64 complex per row)
+  float* bpart = nullptr;   // [nplanes][3 (G_R, G_I, TVX)][tiles_per_plane]
 };
+
+// the launch's boundary-row statistics come from k_prox_tvfix
+inline bool prox_tvfix_launch(const ProxArgs& a) {
+  return a.tvfix && a.kind == 1 && !a.pass_len && a.tau_tv > 0.f && a.wside && a.bpart;
+}
 
 // Peer-memory spectrum reduction (peer.cu): every rank's symmetric buffers.
 constexpr int kMaxPeers = 8;

@@ -141,7 +141,7 @@ HD Work work_geom(const ProxArgs& a, int work) {
   t.j0 = tx * a.tile;
   t.i1 = min(a.ny, t.i0 + a.tile_h);
   t.j1 = min(a.nx, t.j0 + a.tile);
-  t.ri0 = min(max(t.i0 - a.halo, 0), a.ny - RH);  // region clamped into the plane
+  t.ri0 = min(max(t.i0 - a.halo_y, 0), a.ny - RH);  // region clamped into the plane
   t.rj0 = min(max(t.j0 - a.halo, 0), a.nx - RW);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   wk.g0 = (long long)wk.plane * a.P + (long long)(t.ri0 + w * SR) * a.nx + t.rj0 + 2 * lane;
@@ -366,6 +366,14 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     if (gi >= i0 && gi < i1) rInt |= 1u << s;
   }
   const bool cInt = gj >= j0 && gj < j1;
+  // tvfix (single pass, top halo T): the row above the tile's first row is in
+  // this region's garbage zone, so that row's TV(w) / TV(x_new) terms are left
+  // to k_prox_tvfix (rTV); its pointwise terms stay here (rInt)
+  uint32_t rTV = rInt;
+  if constexpr (TV && !WALK) {
+    const int rf = i0 - ri0 - r0;
+    if (a.tvfix && i0 > 0 && rf >= 0 && rf < SR) rTV &= ~(1u << rf);
+  }
   const long long g0 = wk.g0;
   constexpr bool staged = PH <= 1;
   // Staged kernels keep x and grad double-buffered ([buf][x, grad]) and x_prev
@@ -517,6 +525,22 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     }
     if (rInt & (1u << s)) acc[PT_L1] += l1;
   }
+  };
+  // tvfix: w (after the guard's identity parts) of the tile's first and last
+  // rows for k_prox_tvfix, 64 region columns per row
+  auto save_wside = [&]() {
+    if constexpr (TV && !WALK) {
+      if (a.tvfix) {
+        const int rf = i0 - ri0 - r0, rl = i1 - 1 - ri0 - r0;
+        float4* ws = a.wside + (long long)(plane * a.tiles_per_plane + tile) * 64 + lane;
+        HOLO_DCHECK(plane * a.tiles_per_plane + tile < a.nplanes * a.tiles_per_plane, CK_PROX_STORE);
+#pragma unroll
+        for (int s = 0; s < SR; ++s) {
+          if (s == rf) ws[0] = f4(rp[s][0], rp[s][1]);
+          if (s == rl) ws[32] = f4(rp[s][0], rp[s][1]);
+        }
+      }
+    }
   };
   if (TV) {
     const float2 lr2 = splat2(a.lr_tv);
@@ -718,6 +742,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         }
       }
       soft_rows();
+      save_wside();
       // Last rows of w and x_new for the band below, in top[0] / top[1]: every
       // band's reads of the band slots ended before its final-sweep arrival,
       // and the next region writes top[] only behind its iteration-0 barrier
@@ -741,7 +766,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
           up0 = rp[s][0];
           up1 = rp[s][1];
           if (rInt & (1u << s)) {
-            const float2 nw = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
+            const float2 nw = (rTV & (1u << s)) ? add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1)) : make_float2(0.f, 0.f);
             const float2 d0 = sub2(rp[s][0], v[s][0]), d1 = sub2(rp[s][1], v[s][1]);
             const float2 dd = fma2(d0, d0, mul2(d1, d1));
             acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f, dd.x, acc[PT_G_R]));
@@ -769,6 +794,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
     save_rows(kSaveW, rp);
     fetch_above(0, kSaveW);
     soft_rows();  // x_new -> p: needs only this band's w, so it runs ahead of the barrier
+    save_wside();
     __syncthreads();
     // guard statistics: tau TV(w) + |w - v|^2 / 2 against tau TV(v)
     {
@@ -781,7 +807,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
         up0 = rp[s][0];
         up1 = rp[s][1];
         if (rInt & (1u << s)) {
-          const float2 nw = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
+          const float2 nw = (rTV & (1u << s)) ? add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1)) : make_float2(0.f, 0.f);
           const float2 d0 = sub2(rp[s][0], v[s][0]), d1 = sub2(rp[s][1], v[s][1]);
           const float2 dd = fma2(d0, d0, mul2(d1, d1));  // (re, im) |w - v|^2 of the pair
           acc[PT_G_R] = fmaf(ttv, nw.x, fmaf(0.5f, dd.x, acc[PT_G_R]));
@@ -836,7 +862,7 @@ __device__ __forceinline__ void prox_tile(const ProxArgs& a, const TmaMaps& maps
       up1 = p[s][1];
       if (!(rInt & (1u << s))) continue;
       const long long g = g0 + (long long)s * a.nx;
-      {
+      if (rTV & (1u << s)) {
         const float2 nx2 = add2(norm_pair(gy0, gx0), norm_pair(gy1, gx1));
         acc[PT_TVX] += nx2.x + nx2.y;
       }
@@ -1084,13 +1110,29 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   // multi-pass: strip walk, only the frame bottom is halo (Tp A-steps + the
   // final D^T); single pass: square tiles with halo on every side
   a.walk = tp > 0 && !getenv("HOLO_PROX_NOWALK");
+  a.tvfix = 0;
   if (a.walk) {
     a.tile_h = (RH - (tp + 1)) / SR * SR;  // multiple of SR: the saved row ends a band
     a.ky = ny > RH ? 1 + (ny - RH + a.tile_h - 1) / a.tile_h : 1;
   } else {
     a.tile_h = RH - h_lo - h_hi;
     a.ky = (ny + a.tile_h - 1) / a.tile_h;
+    // tvfix: top halo T instead of T + 1 (w / x_new are valid from row T of a
+    // region; only the TV terms of a tile's first row reach one row higher,
+    // and k_prox_tvfix takes those from the neighbouring tile), bottom T:
+    // 54-row tiles at T = 5, used where that saves a tile row (1024 rows: 19
+    // instead of 20 region rows).  HOLO_PROX_TVFIX=1 / 0 forces it on / off.
+    const char* tf = getenv("HOLO_PROX_TVFIX");
+    const int th2 = RH - 2 * inner, ky2 = (ny + th2 - 1) / th2;
+    const bool fix = tf ? tf[0] == '1' : ky2 < a.ky;
+    if (fix && ny > RH) {
+      a.tvfix = 1;
+      a.halo_y = inner;
+      a.tile_h = th2;
+      a.ky = ky2;
+    }
   }
+  if (!a.tvfix) a.halo_y = a.halo;
   a.rcp_ky = 1.f / (float)a.ky;
   a.tiles_per_plane = a.tiles_x * a.ky;
   a.rcp_tx = 1.f / (float)a.tiles_x;
@@ -1110,7 +1152,7 @@ void prox_strip_setup(ProxArgs& a, int ny, int nx, int inner) {
   a.icnt = 0;
   if (!a.walk) {
     interior(a.tiles_x, a.tile, a.halo, nx, RW, a.ix0, a.ix1);
-    interior(a.ky, a.tile_h, a.halo, ny, RH, a.iy0, a.iy1);
+    interior(a.ky, a.tile_h, a.halo_y, ny, RH, a.iy0, a.iy1);
     a.icnt = (a.ix1 - a.ix0) * (a.iy1 - a.iy0);
   }
   if (a.icnt > 0) {
