@@ -2,7 +2,7 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -DHOLO_WITH_NCCL --expt-relaxed-constexpr $(EXTRA)
-SRC := paper_1904_04884_b200/csrc/kernels.cu paper_1904_04884_b200/csrc/prox_strip.cu paper_1904_04884_b200/csrc/engine.cu paper_1904_04884_b200/csrc/segment.cu paper_1904_04884_b200/csrc/synth.cu paper_1904_04884_b200/csrc/peer.cu
+SRC := paper_1904_04884_b200/csrc/kernels.cu paper_1904_04884_b200/csrc/prox_strip.cu paper_1904_04884_b200/csrc/engine.cu paper_1904_04884_b200/csrc/segment.cu paper_1904_04884_b200/csrc/synth.cu paper_1904_04884_b200/csrc/peer.cu paper_1904_04884_b200/csrc/gfft.cu
 HDR := $(wildcard paper_1904_04884_b200/csrc/*.cuh) include/holo_b200.h
 LIB := paper_1904_04884_b200/libholo_b200.so
 OBJ := $(patsubst paper_1904_04884_b200/csrc/%.cu,build/%.o,$(SRC))

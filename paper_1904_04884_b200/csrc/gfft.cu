@@ -1,0 +1,295 @@
+// General plane sizes: mixed-radix transforms for planes whose sides are not
+// powers of two (the reference's numpy FFTs take any size, optics.py:119-122,
+// solver.py:117-132).  The power-of-two path (fft.cuh, the fused TMA column
+// passes) stays the production path; a plane with a side that is not a power
+// of two runs every pass through the kernels below instead, with the same
+// semantics as fft_rows / fft_cols / adj_cols / fwd_cols (kernels.cuh):
+//
+//  * each line (row or column) is transformed in shared memory by a Stockham
+//    autosort over the prime factors of N (radix 4 for pairs of 2s): stage
+//    (R, Ns) maps butterfly j to outputs (j / Ns) Ns R + j % Ns + q Ns with the
+//    combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)) from one fp64-exact
+//    table of the N roots of unity, so every butterfly is R^2 table MACs
+//    (largest admitted prime factor: kMaxPrime);
+//  * the adjoint multiplies R by the plane weight U_k on the load (complex
+//    engine: H_{k0+k}; packed real engine: Re H_j + i Re H_{j+1}, j = k0 + 2k),
+//    the forward accumulates colFFT(v_k) conj(U_k) over a CTA's plane group in
+//    shared memory (no Horner recurrence: U_k is evaluated exactly per plane
+//    from the 64-bit phase), all-zero planes (live[k] == 0) skipped.
+//
+// Throughput is not the point of this path (the lines are smem-latency bound);
+// it exists so that any camera frame (1000x1000, 1280x1024, ...) reconstructs
+// on the GPU with the reference's results.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace holo {
+
+namespace {
+
+constexpr int kGThreads = 256;
+constexpr int kGLineElems = 4096;  // elements per CTA (lines x N)
+
+struct Radices {
+  int n = 0;
+  int r[24] = {};
+};
+
+Radices factor(int N) {
+  Radices f;
+  int n = N;
+  while (n % 4 == 0 && n > 4) { f.r[f.n++] = 4; n /= 4; }
+  for (int p = 2; n > 1; ++p)
+    while (n % p == 0) { f.r[f.n++] = p; n /= p; }
+  return f;
+}
+
+int largest_prime(int N) {
+  int best = 1, n = N;
+  for (int p = 2; n > 1; ++p)
+    while (n % p == 0) { best = p; n /= p; }
+  return best;
+}
+
+// W[m] = exp(-2 pi i m / N), fp64 argument reduced exactly
+__global__ void k_groots(float2* W, int N) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N) return;
+  double s, c;
+  sincospi(-2.0 * (double)m / (double)N, &s, &c);
+  W[m] = make_float2((float)c, (float)s);
+}
+
+// L lines of N points in a (line-major [L][N]); returns the buffer holding the result
+__device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& rad, const float2* W, bool inv) {
+  float2* src = a;
+  float2* dst = b;
+  int Ns = 1;
+  for (int s = 0; s < rad.n; ++s) {
+    const int R = rad.r[s], M = N / R, step = N / (Ns * R);
+    for (int t = threadIdx.x; t < L * M; t += blockDim.x) {
+      const int line = t / M, j = t - line * M;
+      const float2* sl = src + line * N;
+      float2* dl = dst + line * N;
+      const int jm = j % Ns, base = (j / Ns) * Ns * R + jm;
+      for (int q = 0; q < R; ++q) {
+        const int e = (jm + q * Ns) * step;  // < N
+        float2 acc = czero();
+        int m = 0;
+        for (int r = 0; r < R; ++r) {
+          const float2 x = sl[j + r * M];
+          float2 w = W[m];
+          if (inv) w.y = -w.y;
+          acc = make_float2(fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x)), fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y)));
+          m += e;
+          if (m >= N) m -= N;
+        }
+        dl[base + q * Ns] = acc;
+      }
+    }
+    __syncthreads();
+    float2* t = src;
+    src = dst;
+    dst = t;
+    Ns *= R;
+  }
+  return src;
+}
+
+__device__ void load_roots(float2* Ws, const float2* Wg, int N) {
+  for (int i = threadIdx.x; i < N; i += blockDim.x) Ws[i] = Wg[i];
+}
+
+// plane weight U_k at pixel phase t (see the file comment)
+__device__ float2 plane_weight(uint64_t t, int k0, int k, bool packed, const float2* circ) {
+  if (packed) {
+    const int j = k0 + 2 * k;
+    return make_float2(cis_cycles(plane_phase(t, j), circ).x, cis_cycles(plane_phase(t, j + 1), circ).x);
+  }
+  return cis_cycles(plane_phase(t, k0 + k), circ);
+}
+
+// rows: CTA = L consecutive rows of N = nx points
+__global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* out, long long nrows, int N, int L,
+                                                     Radices rad, const float2* __restrict__ Wg, bool inv,
+                                                     float scale, const uint8_t* __restrict__ live,
+                                                     int rows_per_plane) {
+  extern __shared__ __align__(16) float2 gsm[];
+  float2* W = gsm;
+  float2* a = gsm + N;
+  float2* b = a + (size_t)L * N;
+  load_roots(W, Wg, N);
+  const long long r0 = (long long)blockIdx.x * L;
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+    const long long row = r0 + t / N;
+    const bool on = row < nrows && !(live && !live[row / rows_per_plane]);
+    a[t] = on ? in[r0 * N + t] : czero();
+  }
+  __syncthreads();
+  const float2* res = stockham(a, b, N, L, rad, W, inv);
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+    const long long row = r0 + t / N;
+    if (row < nrows && !(live && !live[row / rows_per_plane])) out[r0 * N + t] = cscale(res[t], scale);
+  }
+}
+
+// columns: CTA = L adjacent columns of one plane (blockIdx.y), N = ny points.
+// mode 0: out[k] = scale * colFFT(in[k]); mode 1 (adjoint): out[k] = colIFFT(U_k R)
+__global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* out, int nx, int N, int L, Radices rad,
+                                                     const float2* __restrict__ Wg, bool inv, float scale, int mode,
+                                                     const uint64_t* __restrict__ tab,
+                                                     const float2* __restrict__ circ, int k0, bool packed) {
+  extern __shared__ __align__(16) float2 gsm[];
+  float2* W = gsm;
+  float2* a = gsm + N;
+  float2* b = a + (size_t)L * N;
+  load_roots(W, Wg, N);
+  const int c0 = blockIdx.x * L, k = blockIdx.y;
+  const long long P = (long long)nx * N;
+  const float2* src = mode == 1 ? in : in + (long long)k * P;
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+    const int l = t % L, i = t / L, c = c0 + l;
+    float2 v = czero();
+    if (c < nx) {
+      const long long p = (long long)i * nx + c;
+      v = src[p];
+      if (mode == 1) v = cmul(v, plane_weight(tab[p], k0, k, packed, circ));
+    }
+    a[l * N + i] = v;
+  }
+  __syncthreads();
+  const float2* res = stockham(a, b, N, L, rad, W, inv);
+  float2* dst = out + (long long)k * P;
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+    const int l = t % L, i = t / L, c = c0 + l;
+    if (c < nx) dst[(long long)i * nx + c] = cscale(res[l * N + i], scale);
+  }
+}
+
+// forward: Spart[g] = sum_{k in group g, live} colFFT(in[k]) conj(U_k)
+__global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Spart, int nx, int N, int L, Radices rad,
+                                                    const float2* __restrict__ Wg, int nzl, int ppg,
+                                                    const uint64_t* __restrict__ tab,
+                                                    const float2* __restrict__ circ, int k0, bool packed,
+                                                    const uint8_t* __restrict__ live) {
+  extern __shared__ __align__(16) float2 gsm[];
+  float2* W = gsm;
+  float2* a = gsm + N;
+  float2* b = a + (size_t)L * N;
+  float2* acc = b + (size_t)L * N;
+  load_roots(W, Wg, N);
+  const int c0 = blockIdx.x * L, kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
+  const long long P = (long long)nx * N;
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) acc[t] = czero();
+  for (int k = kb; k < ke; ++k) {
+    if (live && !live[k]) continue;
+    __syncthreads();  // the previous plane's accumulate read its result buffer
+    for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+      const int l = t % L, i = t / L, c = c0 + l;
+      a[l * N + i] = c < nx ? in[(long long)k * P + (long long)i * nx + c] : czero();
+    }
+    __syncthreads();
+    const float2* res = stockham(a, b, N, L, rad, W, false);
+    for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+      const int l = t % L, i = t / L, c = c0 + l;
+      if (c < nx) {
+        const float2 u = plane_weight(tab[(long long)i * nx + c], k0, k, packed, circ);
+        const float2 v = res[l * N + i];
+        // v conj(u)
+        acc[l * N + i] = cadd(acc[l * N + i], make_float2(v.x * u.x + v.y * u.y, v.y * u.x - v.x * u.y));
+      }
+    }
+  }
+  __syncthreads();
+  float2* dst = Spart + (long long)blockIdx.y * P;
+  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+    const int l = t % L, i = t / L, c = c0 + l;
+    if (c < nx) dst[(long long)i * nx + c] = acc[l * N + i];
+  }
+}
+
+int lines_per_cta(int N) { return std::max(1, std::min(16, kGLineElems / N)); }
+
+size_t smem_bytes(int N, int L, int bufs) { return sizeof(float2) * ((size_t)N + (size_t)bufs * L * N); }
+
+template <class K>
+cudaError_t allow_smem(K kern, size_t bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+bool pow2_side(int n) { return n >= 8 && n <= 4096 && (n & (n - 1)) == 0; }
+
+bool generic_side(int n) { return n >= 8 && n <= 4096 && largest_prime(n) <= kMaxPrime; }
+
+cudaError_t gplan_build(Plan& p, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaMalloc(&p.groots_x, sizeof(float2) * p.nx))) return e;
+  if ((e = cudaMalloc(&p.groots_y, sizeof(float2) * p.ny))) return e;
+  k_groots<<<(p.nx + 255) / 256, 256, 0, s>>>(p.groots_x, p.nx);
+  k_groots<<<(p.ny + 255) / 256, 256, 0, s>>>(p.groots_y, p.ny);
+  add_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t g_fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
+                       cudaStream_t s, const uint8_t* live, int rows_per_plane) {
+  const int N = p.nx, L = lines_per_cta(N);
+  const size_t smem = smem_bytes(N, L, 2);
+  cudaError_t e = allow_smem(k_grows, smem);
+  if (e) return e;
+  const long long blocks = (nrows + L - 1) / L;
+  if (blocks <= 0) return cudaSuccess;
+  k_grows<<<(unsigned)blocks, kGThreads, smem, s>>>(in, out, nrows, N, L, factor(N), p.groots_x, inverse, scale, live,
+                                                    std::max(rows_per_plane, 1));
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t g_fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
+                       cudaStream_t s) {
+  const int N = p.ny, L = lines_per_cta(N);
+  const size_t smem = smem_bytes(N, L, 2);
+  cudaError_t e = allow_smem(k_gcols, smem);
+  if (e) return e;
+  if (nplanes <= 0) return cudaSuccess;
+  dim3 grid((p.nx + L - 1) / L, nplanes);
+  k_gcols<<<grid, kGThreads, smem, s>>>(in, out, p.nx, N, L, factor(N), p.groots_y, inverse, scale, 0, p.phase,
+                                        p.circle, 0, false);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t g_adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed) {
+  const int N = p.ny, L = lines_per_cta(N);
+  const size_t smem = smem_bytes(N, L, 2);
+  cudaError_t e = allow_smem(k_gcols, smem);
+  if (e) return e;
+  if (nzl <= 0) return cudaSuccess;
+  dim3 grid((p.nx + L - 1) / L, nzl);
+  k_gcols<<<grid, kGThreads, smem, s>>>(R, out, p.nx, N, L, factor(N), p.groots_y, true, 1.0f, 1, p.phase, p.circle,
+                                        k0, packed);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t g_fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
+                       bool packed, const uint8_t* live) {
+  const int N = p.ny, L = lines_per_cta(N);
+  const size_t smem = smem_bytes(N, L, 3);
+  cudaError_t e = allow_smem(k_gfwd, smem);
+  if (e) return e;
+  groups = std::max(groups, 1);
+  const int ppg = std::max(1, (nzl + groups - 1) / groups);
+  dim3 grid((p.nx + L - 1) / L, groups);
+  k_gfwd<<<grid, kGThreads, smem, s>>>(in, Spart, p.nx, N, L, factor(N), p.groots_y, nzl, ppg, p.phase, p.circle, k0,
+                                       packed, live);
+  add_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace holo

@@ -1150,10 +1150,13 @@ inline int grid_for(long long n, int threads, int cap = 148 * 16) {
 static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
 #define COUNT_LAUNCH(n) g_launches.fetch_add((n), std::memory_order_relaxed)
+void add_launches(long long n) { COUNT_LAUNCH(n); }
 
 bool plan_supported(int nx, int ny) {
-  auto ok = [](int n) { return n >= 8 && n <= 4096 && (n & (n - 1)) == 0; };
-  return ok(nx) && ok(ny);
+  // powers of two: the fused production passes; other sides: gfft.cu (the
+  // packed strip prox and its tensor maps need an even row: nx even)
+  if (pow2_side(nx) && pow2_side(ny)) return true;
+  return generic_side(nx) && generic_side(ny) && nx % 2 == 0;
 }
 
 cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,
@@ -1162,6 +1165,7 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
   p.P = (long long)nx * ny;
   p.pitch = pitch; p.dz = dz; p.z0 = z0; p.lam = lam;
   p.col_c = col_width(ny);
+  p.generic = (pow2_side(nx) && pow2_side(ny)) ? 0 : 1;
   cudaError_t e;
   for (int k = 0; k < 2; ++k) {
     if ((e = cudaMalloc(&p.tw_x[k], sizeof(float4) * std::max(nx, 32)))) return e;
@@ -1186,6 +1190,7 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
   COUNT_LAUNCH(1);
   k_phase<<<(int)((p.P + 255) / 256), 256, 0, s>>>(p.phase, p.mask, ny, nx, pitch, lam, z0, dz);
   COUNT_LAUNCH(1);
+  if (p.generic && (e = gplan_build(p, s))) return e;
   // the DC sample (fx = fy = 0, arg = 1) always propagates, so ||A||^2 = nz exactly
   p.any_propagating = 1;
   if ((e = cudaStreamSynchronize(s))) return e;
@@ -1193,6 +1198,9 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
 }
 
 void plan_free(Plan& p) {
+  cudaFree(p.groots_x);
+  cudaFree(p.groots_y);
+  p.groots_x = p.groots_y = nullptr;
   for (int k = 0; k < 2; ++k) {
     cudaFree(p.tw_x[k]);
     cudaFree(p.tw_y[k]);
@@ -1215,6 +1223,7 @@ HOLO_CHECK_TU(check_bits_kernels)
 cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
                      cudaStream_t s, const uint8_t* live, int rows_per_plane) {
   if (live && (rows_per_plane <= 0 || nrows >= (1LL << 31))) return cudaErrorInvalidValue;
+  if (p.generic) return g_fft_rows(p, in, out, nrows, inverse, scale, s, live, rows_per_plane);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.nx, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1269,6 +1278,7 @@ static size_t col_smem(int extra) {
 
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
                      cudaStream_t s) {
+  if (p.generic) return g_fft_cols(p, in, out, nplanes, inverse, scale, s);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1310,6 +1320,7 @@ constexpr int kMaxRecur = 32;
 #define HOLO_FWD_C(N) ((N) <= HOLO_FWD_STAGED_MAX ? HOLO_FWD_CC : 4)
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed) {
+  if (p.generic) return g_adj_cols(p, R, out, nzl, k0, s, packed);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1366,6 +1377,7 @@ int fwd_groups(const Plan& p, int nzl) {
 
 cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
                      bool packed, const uint8_t* live) {
+  if (p.generic) return g_fwd_cols(p, in, Spart, nzl, k0, groups, s, packed, live);
   cudaError_t err = cudaSuccess;
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {

@@ -18,6 +18,11 @@ struct Plan {
   uint64_t* phase = nullptr;    // per pixel packed (frac(z0 q), frac(dz q)) cycle fractions (plane_phase)
   uint8_t* mask = nullptr;      // per pixel 1 = propagating (arg >= 0)
   int any_propagating = 0;
+  // general plane sizes (gfft.cu): a side that is not a power of two runs every
+  // pass through the mixed-radix kernels; W_N roots per side
+  int generic = 0;
+  float2* groots_x = nullptr;
+  float2* groots_y = nullptr;
 };
 
 constexpr int kProxParts = 6;  // per-tile fp64 partial sums written by the prox kernel
@@ -97,6 +102,19 @@ cudaError_t peer_gather(long long P, const PeerSet& ps, unsigned long long epoch
 // 2D tiled TMA descriptor over float rows (kernels.cu); nonzero on failure
 int encode_tiled_2d(CUtensorMap* m, const void* base, long long inner, long long rows, int box_inner, int box_rows);
 bool plan_supported(int nx, int ny);
+// gfft.cu: general plane sizes (mixed radix, prime factors <= kMaxPrime)
+constexpr int kMaxPrime = 61;
+bool pow2_side(int n);
+bool generic_side(int n);
+cudaError_t gplan_build(Plan& p, cudaStream_t s);
+cudaError_t g_fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
+                       cudaStream_t s, const uint8_t* live, int rows_per_plane);
+cudaError_t g_fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
+                       cudaStream_t s);
+cudaError_t g_adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed);
+cudaError_t g_fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
+                       bool packed, const uint8_t* live);
+void add_launches(long long n);
 long long launch_count();  // kernels launched by this library since load
 cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,
                        cudaStream_t s);
