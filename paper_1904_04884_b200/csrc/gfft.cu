@@ -9,8 +9,9 @@
 //    autosort over the prime factors of N (radix 4 for pairs of 2s): stage
 //    (R, Ns) maps butterfly j to outputs (j / Ns) Ns R + j % Ns + q Ns with the
 //    combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)) from one fp64-exact
-//    table of the N roots of unity, so every butterfly is R^2 table MACs
-//    (largest admitted prime factor: kMaxPrime);
+//    table of the N roots of unity: a stage twiddle per input, then an
+//    in-register radix-2/3/4 (closed form) or radix-5/7 (table) DFT; larger
+//    prime factors (up to kMaxPrime) re-read their inputs, R^2 table MACs;
 //  * the adjoint multiplies R by the plane weight U_k on the load (complex
 //    engine: H_{k0+k}; packed real engine: Re H_j + i Re H_{j+1}, j = k0 + 2k),
 //    the forward accumulates colFFT(v_k) conj(U_k) over a CTA's plane group in
@@ -63,6 +64,81 @@ __global__ void k_groots(float2* W, int N) {
   W[m] = make_float2((float)c, (float)s);
 }
 
+HD float2 conj_if(float2 w, bool inv) { return inv ? make_float2(w.x, -w.y) : w; }
+
+// In-register butterfly of radix R (R = 2, 3, 4 closed form; others by table):
+// x_r <- x_r W_N^(r jm step) (stage twiddle), then y_q = sum_r x_r W_R^(r q).
+template <int R>
+__device__ __forceinline__ void bfly(const float2* sl, float2* dl, int j, int M, int jm, int Ns, int step, int base,
+                                     const float2* W, bool inv, int N) {
+  float2 x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) x[r] = sl[j + r * M];
+  const int e = jm * step;
+  int m = e;
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    x[r] = cmul(x[r], conj_if(W[m], inv));
+    m += e;
+    if (m >= N) m -= N;
+  }
+  if constexpr (R == 2) {
+    const float2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const float2 a = cadd(x[0], x[2]), b = csub(x[0], x[2]), c = cadd(x[1], x[3]), d = csub(x[1], x[3]);
+    const float2 di = inv ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);  // W_4 d = -+ i d
+    x[0] = cadd(a, c);
+    x[2] = csub(a, c);
+    x[1] = cadd(b, di);
+    x[3] = csub(b, di);
+  } else if constexpr (R == 3) {
+    const float sn = inv ? 0.86602540378443865f : -0.86602540378443865f;  // Im W_3
+    const float2 t = cadd(x[1], x[2]), u = csub(x[1], x[2]);
+    const float2 c = make_float2(fmaf(-0.5f, t.x, x[0].x), fmaf(-0.5f, t.y, x[0].y));
+    const float2 iu = make_float2(-sn * u.y, sn * u.x);
+    x[0] = cadd(x[0], t);
+    x[1] = cadd(c, iu);
+    x[2] = csub(c, iu);
+  } else {
+    float2 y[R];
+    const int nr = N / R;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      float2 acc = x[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const float2 w = conj_if(W[((r * q) % R) * nr], inv);
+        acc = make_float2(fmaf(x[r].x, w.x, fmaf(-x[r].y, w.y, acc.x)), fmaf(x[r].x, w.y, fmaf(x[r].y, w.x, acc.y)));
+      }
+      y[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[q] = y[q];
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) dl[base + q * Ns] = x[q];
+}
+
+// large prime radix: inputs re-read from shared memory, R^2 table MACs
+__device__ void bfly_any(const float2* sl, float2* dl, int j, int M, int jm, int Ns, int step, int base, int R,
+                         const float2* W, bool inv, int N) {
+  for (int q = 0; q < R; ++q) {
+    const int e = (jm + q * Ns) * step;  // < N
+    float2 acc = czero();
+    int m = 0;
+    for (int r = 0; r < R; ++r) {
+      const float2 x = sl[j + r * M];
+      const float2 w = conj_if(W[m], inv);
+      acc = make_float2(fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x)), fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y)));
+      m += e;
+      if (m >= N) m -= N;
+    }
+    dl[base + q * Ns] = acc;
+  }
+}
+
 // L lines of N points in a (line-major [L][N]); returns the buffer holding the result
 __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& rad, const float2* W, bool inv) {
   float2* src = a;
@@ -75,19 +151,13 @@ __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& r
       const float2* sl = src + line * N;
       float2* dl = dst + line * N;
       const int jm = j % Ns, base = (j / Ns) * Ns * R + jm;
-      for (int q = 0; q < R; ++q) {
-        const int e = (jm + q * Ns) * step;  // < N
-        float2 acc = czero();
-        int m = 0;
-        for (int r = 0; r < R; ++r) {
-          const float2 x = sl[j + r * M];
-          float2 w = W[m];
-          if (inv) w.y = -w.y;
-          acc = make_float2(fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x)), fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y)));
-          m += e;
-          if (m >= N) m -= N;
-        }
-        dl[base + q * Ns] = acc;
+      switch (R) {
+        case 2: bfly<2>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+        case 3: bfly<3>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+        case 4: bfly<4>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+        case 5: bfly<5>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+        case 7: bfly<7>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+        default: bfly_any(sl, dl, j, M, jm, Ns, step, base, R, W, inv, N);
       }
     }
     __syncthreads();

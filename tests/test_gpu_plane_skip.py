@@ -93,3 +93,19 @@ def test_real_engine_skipping_is_exact():
                         real=True)
     assert rel_l2(x1, ref.x) <= 1e-4, rel_l2(x1, ref.x)
     assert np.allclose(h1, ref.history, rtol=2e-5, atol=1e-9)
+
+
+def test_skipping_on_general_plane_sides():
+    """The mixed-radix passes (gfft.cu, sides that are not powers of two) skip
+    dead planes exactly like the fused passes."""
+    geom = (120, 96, 16, 10e-6, 100e-6, 2e-3, 632e-9)
+    g = O.Geometry(*geom)
+    pts = O.make_scene(3, g, 40e-6, seed=1, margin_planes=2)
+    b = O.invert_residual(O.render_hologram(pts, g, 40e-6))
+    x1, r1, h1 = _solve(b, 3.0, 0.2, 8, 5, skip=True, geom=geom)
+    x0, r0, h0 = _solve(b, 3.0, 0.2, 8, 5, skip=False, geom=geom)
+    assert r1.skipped_planes > 0 and r0.skipped_planes == 0
+    assert np.array_equal(h1, h0) and np.array_equal(x1, x0)
+    ref = O.fista_solve(b, g, lam_l1=3.0, lam_tv=0.2, max_iters=8, inner=5, step_size=1.0 / 32)
+    assert [k for k in range(16) if not np.any(x1[k])] == [k for k in range(16) if not np.any(ref.x[k])]
+    assert rel_l2(x1, ref.x) <= 1e-4
