@@ -34,10 +34,15 @@ namespace {
 constexpr int kGThreads = 256;
 constexpr int kGLineElems = 4096;  // elements per CTA (lines x N)
 
+// per-stage constants; m*: exact reciprocals for x < 2^12 (q = umulhi(x, m), d >= 2)
 struct Radices {
   int n = 0;
   int r[24] = {};
+  int M[24] = {}, Ns[24] = {}, step[24] = {};
+  unsigned mM[24] = {}, mNs[24] = {};
 };
+
+unsigned magic(int d) { return d >= 2 ? (unsigned)((0x100000000ull + (unsigned long long)d - 1) / (unsigned long long)d) : 0u; }
 
 Radices factor(int N) {
   Radices f;
@@ -45,8 +50,20 @@ Radices factor(int N) {
   while (n % 4 == 0 && n > 4) { f.r[f.n++] = 4; n /= 4; }
   for (int p = 2; n > 1; ++p)
     while (n % p == 0) { f.r[f.n++] = p; n /= p; }
+  int ns = 1;
+  for (int s = 0; s < f.n; ++s) {
+    f.M[s] = N / f.r[s];
+    f.Ns[s] = ns;
+    f.step[s] = N / (ns * f.r[s]);
+    f.mM[s] = magic(f.M[s]);
+    f.mNs[s] = magic(ns);
+    ns *= f.r[s];
+  }
   return f;
 }
+
+// x / d for 0 <= x < 2^12 (d = 1: x)
+__device__ __forceinline__ int udiv(int x, int d, unsigned m) { return d == 1 ? x : (int)__umulhi((unsigned)x, m); }
 
 int largest_prime(int N) {
   int best = 1, n = N;
@@ -143,14 +160,14 @@ __device__ void bfly_any(const float2* sl, float2* dl, int j, int M, int jm, int
 __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& rad, const float2* W, bool inv) {
   float2* src = a;
   float2* dst = b;
-  int Ns = 1;
   for (int s = 0; s < rad.n; ++s) {
-    const int R = rad.r[s], M = N / R, step = N / (Ns * R);
+    const int R = rad.r[s], M = rad.M[s], Ns = rad.Ns[s], step = rad.step[s];
+    const unsigned mM = rad.mM[s], mNs = rad.mNs[s];
     for (int t = threadIdx.x; t < L * M; t += blockDim.x) {
-      const int line = t / M, j = t - line * M;
+      const int line = udiv(t, M, mM), j = t - line * M;
       const float2* sl = src + line * N;
       float2* dl = dst + line * N;
-      const int jm = j % Ns, base = (j / Ns) * Ns * R + jm;
+      const int jq = udiv(j, Ns, mNs), jm = j - jq * Ns, base = jq * Ns * R + jm;
       switch (R) {
         case 2: bfly<2>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
         case 3: bfly<3>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
@@ -164,7 +181,6 @@ __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& r
     float2* t = src;
     src = dst;
     dst = t;
-    Ns *= R;
   }
   return src;
 }
@@ -193,16 +209,17 @@ __global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* o
   float2* b = a + (size_t)L * N;
   load_roots(W, Wg, N);
   const long long r0 = (long long)blockIdx.x * L;
-  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-    const long long row = r0 + t / N;
+  for (int l = 0; l < L; ++l) {
+    const long long row = r0 + l;
     const bool on = row < nrows && !(live && !live[row / rows_per_plane]);
-    a[t] = on ? in[r0 * N + t] : czero();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) a[l * N + i] = on ? in[row * N + i] : czero();
   }
   __syncthreads();
   const float2* res = stockham(a, b, N, L, rad, W, inv);
-  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-    const long long row = r0 + t / N;
-    if (row < nrows && !(live && !live[row / rows_per_plane])) out[r0 * N + t] = cscale(res[t], scale);
+  for (int l = 0; l < L; ++l) {
+    const long long row = r0 + l;
+    if (row < nrows && !(live && !live[row / rows_per_plane]))
+      for (int i = threadIdx.x; i < N; i += blockDim.x) out[row * N + i] = cscale(res[l * N + i], scale);
   }
 }
 
@@ -217,11 +234,12 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
   load_roots(W, Wg, N);
+  const int lgL = __ffs(L) - 1;  // L is a power of two
   const int c0 = blockIdx.x * L, k = blockIdx.y;
   const long long P = (long long)nx * N;
   const float2* src = mode == 1 ? in : in + (long long)k * P;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-    const int l = t % L, i = t / L, c = c0 + l;
+    const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
     float2 v = czero();
     if (c < nx) {
       const long long p = (long long)i * nx + c;
@@ -234,7 +252,7 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
   const float2* res = stockham(a, b, N, L, rad, W, inv);
   float2* dst = out + (long long)k * P;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-    const int l = t % L, i = t / L, c = c0 + l;
+    const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
     if (c < nx) dst[(long long)i * nx + c] = cscale(res[l * N + i], scale);
   }
 }
@@ -251,6 +269,7 @@ __global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Sp
   float2* b = a + (size_t)L * N;
   float2* acc = b + (size_t)L * N;
   load_roots(W, Wg, N);
+  const int lgL = __ffs(L) - 1;  // L is a power of two
   const int c0 = blockIdx.x * L, kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
   const long long P = (long long)nx * N;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) acc[t] = czero();
@@ -258,13 +277,13 @@ __global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Sp
     if (live && !live[k]) continue;
     __syncthreads();  // the previous plane's accumulate read its result buffer
     for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-      const int l = t % L, i = t / L, c = c0 + l;
+      const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
       a[l * N + i] = c < nx ? in[(long long)k * P + (long long)i * nx + c] : czero();
     }
     __syncthreads();
     const float2* res = stockham(a, b, N, L, rad, W, false);
     for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-      const int l = t % L, i = t / L, c = c0 + l;
+      const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
       if (c < nx) {
         const float2 u = plane_weight(tab[(long long)i * nx + c], k0, k, packed, circ);
         const float2 v = res[l * N + i];
@@ -276,12 +295,16 @@ __global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Sp
   __syncthreads();
   float2* dst = Spart + (long long)blockIdx.y * P;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
-    const int l = t % L, i = t / L, c = c0 + l;
+    const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
     if (c < nx) dst[(long long)i * nx + c] = acc[l * N + i];
   }
 }
 
-int lines_per_cta(int N) { return std::max(1, std::min(16, kGLineElems / N)); }
+int lines_per_cta(int N) {  // a power of two (t % L, t / L in the column kernels)
+  int L = 1;
+  while (L < 16 && 2 * L * N <= kGLineElems) L *= 2;
+  return L;
+}
 
 size_t smem_bytes(int N, int L, int bufs) { return sizeof(float2) * ((size_t)N + (size_t)bufs * L * N); }
 
