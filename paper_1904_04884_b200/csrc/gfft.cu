@@ -15,7 +15,7 @@
 //  * the adjoint multiplies R by the plane weight U_k on the load (complex
 //    engine: H_{k0+k}; packed real engine: Re H_j + i Re H_{j+1}, j = k0 + 2k),
 //    the forward accumulates colFFT(v_k) conj(U_k) over a CTA's plane group in
-//    shared memory (no Horner recurrence: U_k is evaluated exactly per plane
+//    registers (no Horner recurrence: U_k is evaluated exactly per plane
 //    from the 64-bit phase), all-zero planes (live[k] == 0) skipped.
 //
 // Throughput is not the point of this path (the lines are smem-latency bound);
@@ -32,7 +32,11 @@ namespace holo {
 namespace {
 
 constexpr int kGThreads = 256;
-constexpr int kGLineElems = 4096;  // elements per CTA (lines x N)
+#ifndef HOLO_GLINE
+#define HOLO_GLINE 4096  // 2048 (more CTAs per SM, half-sector column segments) measured 7-20 % slower
+#endif
+constexpr int kGLineElems = HOLO_GLINE;  // target elements per CTA (lines x N; one line if N is larger)
+constexpr int kGMaxN = 4096;
 
 // per-stage constants; m*: exact reciprocals for x < 2^12 (q = umulhi(x, m), d >= 2)
 struct Radices {
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
 }
 
 // forward: Spart[g] = sum_{k in group g, live} colFFT(in[k]) conj(U_k)
-__global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Spart, int nx, int N, int L, Radices rad,
+__global__ void __launch_bounds__(kGThreads, 3) k_gfwd(const float2* in, float2* Spart, int nx, int N, int L, Radices rad,
                                                     const float2* __restrict__ Wg, int nzl, int ppg,
                                                     const uint64_t* __restrict__ tab,
                                                     const float2* __restrict__ circ, int k0, bool packed,
@@ -267,12 +271,15 @@ __global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Sp
   float2* W = gsm;
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
-  float2* acc = b + (size_t)L * N;
   load_roots(W, Wg, N);
   const int lgL = __ffs(L) - 1;  // L is a power of two
   const int c0 = blockIdx.x * L, kb = blockIdx.y * ppg, ke = min(nzl, kb + ppg);
   const long long P = (long long)nx * N;
-  for (int t = threadIdx.x; t < L * N; t += blockDim.x) acc[t] = czero();
+  // the plane sum stays in registers: thread owns elements t = threadIdx.x + n blockDim.x
+  constexpr int kAcc = (kGLineElems > kGMaxN ? kGLineElems : kGMaxN) / kGThreads;
+  float2 acc[kAcc];
+#pragma unroll
+  for (int n = 0; n < kAcc; ++n) acc[n] = czero();
   for (int k = kb; k < ke; ++k) {
     if (live && !live[k]) continue;
     __syncthreads();  // the previous plane's accumulate read its result buffer
@@ -282,21 +289,23 @@ __global__ void __launch_bounds__(kGThreads) k_gfwd(const float2* in, float2* Sp
     }
     __syncthreads();
     const float2* res = stockham(a, b, N, L, rad, W, false);
-    for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+#pragma unroll
+    for (int n = 0; n < kAcc; ++n) {
+      const int t = threadIdx.x + n * kGThreads;
       const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
-      if (c < nx) {
+      if (t < L * N && c < nx) {
         const float2 u = plane_weight(tab[(long long)i * nx + c], k0, k, packed, circ);
         const float2 v = res[l * N + i];
-        // v conj(u)
-        acc[l * N + i] = cadd(acc[l * N + i], make_float2(v.x * u.x + v.y * u.y, v.y * u.x - v.x * u.y));
+        acc[n] = cadd(acc[n], make_float2(v.x * u.x + v.y * u.y, v.y * u.x - v.x * u.y));  // v conj(u)
       }
     }
   }
-  __syncthreads();
   float2* dst = Spart + (long long)blockIdx.y * P;
-  for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+#pragma unroll
+  for (int n = 0; n < kAcc; ++n) {
+    const int t = threadIdx.x + n * kGThreads;
     const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
-    if (c < nx) dst[(long long)i * nx + c] = acc[l * N + i];
+    if (t < L * N && c < nx) dst[(long long)i * nx + c] = acc[n];
   }
 }
 
@@ -373,7 +382,7 @@ cudaError_t g_adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int
 cudaError_t g_fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
                        bool packed, const uint8_t* live) {
   const int N = p.ny, L = lines_per_cta(N);
-  const size_t smem = smem_bytes(N, L, 3);
+  const size_t smem = smem_bytes(N, L, 2);
   cudaError_t e = allow_smem(k_gfwd, smem);
   if (e) return e;
   groups = std::max(groups, 1);

@@ -60,3 +60,46 @@ def test_fista_general_sizes_vs_oracle(shape, inner, real):
     assert rep.iterations == ref.iterations and rep.restarts == ref.restarts
     assert np.allclose(rep.objective, ref.history, rtol=2e-5, atol=1e-9)
     assert rel_l2(vol.to_dense(), ref.x) <= 1e-4
+
+
+@pytest.mark.parametrize("nranks,real", [(2, False), (3, True)])
+def test_rank_group_general_sizes(nranks, real):
+    """z-sharded engine (in-process rank group, peer-memory plane sum over a
+    P that is not a power of two) on a 100x72 geometry: identical decisions
+    and the unsharded volume."""
+    import threading
+    from paper_1904_04884_b200 import RegularizerWeights, VolumeGeometry, estimate_operator_norm
+    from paper_1904_04884_b200.engine import HoloEngine
+    from paper_1904_04884_b200.solver import SolverConfig, native_config
+    g = VolumeGeometry(100, 72, 6, 10e-6, 10e-6, 5e-3, 632e-9)
+    og = O.Geometry.of(g)
+    pts = O.make_scene(6, og, 30e-6, seed=5)
+    b = np.ascontiguousarray(O.invert_residual(O.add_noise(O.render_hologram(pts, og, 30e-6), 0.01, seed=1)))
+    step = 1.0 / (2.0 * estimate_operator_norm(g, real=True)) if real else None
+    cfg = native_config(SolverConfig(weights=RegularizerWeights(0.05, 0.1), max_iters=12, tv_inner_iters=5,
+                                     real_nonnegative=real, step_size=step))
+    group = HoloEngine.local_group(g, nranks)
+    out, errs = [None] * nranks, []
+
+    def run(r):
+        try:
+            out[r] = group[r].solve(b, cfg)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    plain = HoloEngine(g)
+    _, rp, hp = plain.solve(b, cfg)
+    for _, rs, hs in out:
+        assert (rs.iterations, rs.restarts) == (rp.iterations, rp.restarts)
+        assert np.allclose(hs, hp, rtol=1e-5)
+    xs = np.concatenate([e.solution_dense().cpu().numpy() for e in group])
+    assert rel_l2(xs, plain.solution_dense().cpu().numpy()) < 1e-5
+    for e in group:
+        e.close()
+    plain.close()
