@@ -1153,10 +1153,10 @@ long long launch_count() { return g_launches.load(); }
 void add_launches(long long n) { COUNT_LAUNCH(n); }
 
 bool plan_supported(int nx, int ny) {
-  // powers of two: the fused production passes; other sides: gfft.cu (the
-  // packed strip prox and its tensor maps need an even row: nx even)
+  // powers of two: the fused production passes; other sides: gfft.cu (an odd
+  // nx runs the generic tile prox: the strip prox's tensor maps need even rows)
   if (pow2_side(nx) && pow2_side(ny)) return true;
-  return generic_side(nx) && generic_side(ny) && nx % 2 == 0;
+  return generic_side(nx) && generic_side(ny);
 }
 
 cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz, double z0, double lam,

@@ -11,7 +11,8 @@ from oracle import holo_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("nx,ny", [(96, 80), (100, 100), (210, 126), (1280, 24), (24, 1080), (122, 61), (1000, 8)])
+@pytest.mark.parametrize("nx,ny", [(96, 80), (100, 100), (210, 126), (1280, 24), (24, 1080), (122, 61), (1000, 8),
+                                   (99, 35)])
 def test_fft2_general_sizes(nx, ny):
     from paper_1904_04884_b200 import VolumeGeometry
     from paper_1904_04884_b200.engine import HoloEngine
@@ -43,6 +44,8 @@ def test_forward_adjoint_general_sizes_vs_oracle(nx, ny, nz):
                                               ((96, 80, 3), 13, False),    # multi-pass strip walk
                                               ((40, 24, 3), 5, False),     # generic prox (planes < 64)
                                               ((100, 72, 3), 5, True),     # packed real engine, odd nz
+                                              ((99, 70, 3), 5, False),     # odd nx: generic tile prox
+                                              ((75, 66, 3), 13, True),     # odd nx, real engine, T = 13
                                               ((1000, 1000, 2), 5, False)])  # a 1000x1000 camera frame
 def test_fista_general_sizes_vs_oracle(shape, inner, real):
     from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, VolumeGeometry, fista

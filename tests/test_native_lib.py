@@ -24,9 +24,9 @@ def test_version_and_shape_support():
         assert lib.holo_shape_supported(n, n) == 1
     assert lib.holo_shape_supported(1024, 256) == 1
     # general sides (mixed radix, gfft.cu): camera frames, odd ny
-    for nx, ny in ((96, 64), (100, 100), (1280, 1024), (1000, 1000), (1920, 1080), (64, 99), (2 * 61, 64)):
+    for nx, ny in ((96, 64), (100, 100), (1280, 1024), (1000, 1000), (1920, 1080), (64, 99), (99, 64), (2 * 61, 64)):
         assert lib.holo_shape_supported(nx, ny) == 1, (nx, ny)
-    for bad in (4, 8192, 0, 99, 2 * 67):  # too small / large, odd row, prime factor > 61
+    for bad in (4, 8192, 0, 2 * 67, 4099):  # too small / large, prime factor > 61
         assert lib.holo_shape_supported(bad, 64) == 0
     assert lib.holo_shape_supported(64, 67 * 3) == 0
 
