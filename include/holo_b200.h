@@ -79,8 +79,7 @@ int holo_version(void);
  * counterpart: compute-sanitizer substitute for test infrastructure. */
 int holo_debug_checks(uint32_t* bits);
 /* 1 if this build handles the plane shape: sides 8..4096; powers of two run the
- * fused production passes, other sides (prime factors <= 61) the mixed-radix
- * passes of gfft.cu */
+ * fused production passes, any other side the mixed-radix passes of gfft.cu */
 int holo_shape_supported(int32_t nx, int32_t ny);
 
 /* Handle lifecycle.  holo_create: whole volume on one GPU.

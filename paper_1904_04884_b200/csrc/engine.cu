@@ -454,7 +454,7 @@ struct Engine {
     if (g.z0 < 0) return fail(HOLO_ERR_INVALID, "z0 must be nonnegative");
     if (!plan_supported(g.nx, g.ny))
       return fail(HOLO_ERR_UNSUPPORTED, "plane shape " + std::to_string(g.ny) + "x" + std::to_string(g.nx) +
-                                            " unsupported: sides in [8, 4096] with prime factors <= " + std::to_string(kMaxPrime));
+                                            " unsupported: plane sides must lie in [8, 4096]");
     if (n < 1 || r < 0 || r >= n) return fail(HOLO_ERR_INVALID, "bad rank/nranks");
     // every rank owns >= 1 plane: an empty shard would launch zero-sized grids
     if (n > g.nz) return fail(HOLO_ERR_INVALID, "more ranks (" + std::to_string(n) + ") than planes (" +

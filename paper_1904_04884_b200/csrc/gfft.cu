@@ -11,7 +11,8 @@
 //    combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)) from one fp64-exact
 //    table of the N roots of unity: a stage twiddle per input, then an
 //    in-register radix-2/3/4 (closed form) or radix-5/7 (table) DFT; larger
-//    prime factors (up to kMaxPrime) re-read their inputs, R^2 table MACs;
+//    prime factors re-read their inputs, R^2 table MACs (a prime side is a
+//    direct DFT of its lines);
 //  * the adjoint multiplies R by the plane weight U_k on the load (complex
 //    engine: H_{k0+k}; packed real engine: Re H_j + i Re H_{j+1}, j = k0 + 2k),
 //    the forward accumulates colFFT(v_k) conj(U_k) over a CTA's plane group in

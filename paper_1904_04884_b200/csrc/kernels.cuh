@@ -102,8 +102,9 @@ cudaError_t peer_gather(long long P, const PeerSet& ps, unsigned long long epoch
 // 2D tiled TMA descriptor over float rows (kernels.cu); nonzero on failure
 int encode_tiled_2d(CUtensorMap* m, const void* base, long long inner, long long rows, int box_inner, int box_rows);
 bool plan_supported(int nx, int ny);
-// gfft.cu: general plane sizes (mixed radix, prime factors <= kMaxPrime)
-constexpr int kMaxPrime = 61;
+// gfft.cu: general plane sizes (mixed radix; a prime factor above 7 costs R^2
+// table MACs per R outputs, so a prime side is a direct DFT of its lines)
+constexpr int kMaxPrime = 4096;
 bool pow2_side(int n);
 bool generic_side(int n);
 cudaError_t gplan_build(Plan& p, cudaStream_t s);

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("nx,ny", [(96, 80), (100, 100), (210, 126), (1280, 24), (24, 1080), (122, 61), (1000, 8),
-                                   (99, 35)])
+                                   (99, 35), (1021, 8), (134, 67)])
 def test_fft2_general_sizes(nx, ny):
     from paper_1904_04884_b200 import VolumeGeometry
     from paper_1904_04884_b200.engine import HoloEngine
@@ -20,9 +20,19 @@ def test_fft2_general_sizes(nx, ny):
     rng = np.random.default_rng(nx * 31 + ny)
     x = rng.standard_normal((2, ny, nx)) + 1j * rng.standard_normal((2, ny, nx))
     f = eng.fft2(x)
-    assert rel_l2(f, np.fft.fft2(x)) < 3e-6
-    assert rel_l2(eng.fft2(f, inverse=True), x) < 3e-6
+    tol = 3e-6 if max(nx, ny) <= 2048 and all(_largest_prime(n) <= 7 for n in (nx, ny)) else 2e-5  # direct DFTs
+    assert rel_l2(f, np.fft.fft2(x)) < tol
+    assert rel_l2(eng.fft2(f, inverse=True), x) < tol
     eng.close()
+
+
+def _largest_prime(n):
+    best, p = 1, 2
+    while n > 1:
+        while n % p == 0:
+            best, n = p, n // p
+        p += 1
+    return best
 
 
 @pytest.mark.parametrize("nx,ny,nz", [(100, 60, 5), (96, 200, 3), (1280, 40, 2)])
@@ -46,6 +56,7 @@ def test_forward_adjoint_general_sizes_vs_oracle(nx, ny, nz):
                                               ((100, 72, 3), 5, True),     # packed real engine, odd nz
                                               ((99, 70, 3), 5, False),     # odd nx: generic tile prox
                                               ((75, 66, 3), 13, True),     # odd nx, real engine, T = 13
+                                              ((134, 67, 2), 5, False),    # prime factors 67 (direct DFT lines)
                                               ((1000, 1000, 2), 5, False)])  # a 1000x1000 camera frame
 def test_fista_general_sizes_vs_oracle(shape, inner, real):
     from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, VolumeGeometry, fista

@@ -24,11 +24,12 @@ def test_version_and_shape_support():
         assert lib.holo_shape_supported(n, n) == 1
     assert lib.holo_shape_supported(1024, 256) == 1
     # general sides (mixed radix, gfft.cu): camera frames, odd ny
-    for nx, ny in ((96, 64), (100, 100), (1280, 1024), (1000, 1000), (1920, 1080), (64, 99), (99, 64), (2 * 61, 64)):
+    for nx, ny in ((96, 64), (100, 100), (1280, 1024), (1000, 1000), (1920, 1080), (64, 99), (99, 64), (2 * 61, 64),
+                   (2 * 67, 64), (4093, 8)):
         assert lib.holo_shape_supported(nx, ny) == 1, (nx, ny)
-    for bad in (4, 8192, 0, 2 * 67, 4099):  # too small / large, prime factor > 61
+    for bad in (4, 7, 8192, 0, 4099):  # sides outside [8, 4096]
         assert lib.holo_shape_supported(bad, 64) == 0
-    assert lib.holo_shape_supported(64, 67 * 3) == 0
+    assert lib.holo_shape_supported(64, 5000) == 0
 
 
 def test_invalid_arguments_are_status_codes_not_crashes():
@@ -38,7 +39,7 @@ def test_invalid_arguments_are_status_codes_not_crashes():
     g = nat.Geometry(64, 64, 0, 1e-5, 1e-5, 5e-3, 632e-9)
     assert lib.holo_create(ctypes.byref(g), 0, ctypes.byref(h)) == nat.HOLO_ERR_INVALID
     assert "voxel counts" in nat.last_error()
-    g = nat.Geometry(2 * 67, 64, 4, 1e-5, 1e-5, 5e-3, 632e-9)
+    g = nat.Geometry(8192, 64, 4, 1e-5, 1e-5, 5e-3, 632e-9)
     assert lib.holo_create(ctypes.byref(g), 0, ctypes.byref(h)) == nat.HOLO_ERR_UNSUPPORTED
     with pytest.raises(ValueError):
         nat.check(nat.HOLO_ERR_UNSUPPORTED)
