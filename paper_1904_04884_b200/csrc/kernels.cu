@@ -1165,7 +1165,11 @@ cudaError_t plan_build(Plan& p, int nx, int ny, int nz, double pitch, double dz,
   p.P = (long long)nx * ny;
   p.pitch = pitch; p.dz = dz; p.z0 = z0; p.lam = lam;
   p.col_c = col_width(ny);
-  p.generic = (pow2_side(nx) && pow2_side(ny)) ? 0 : 1;
+  // a power-of-two side keeps its fused passes when the other side is general
+  // (1280x1024: fused TMA columns, mixed-radix rows)
+  p.generic_x = pow2_side(nx) ? 0 : 1;
+  p.generic_y = (pow2_side(ny) && nx % 8 == 0) ? 0 : 1;
+  p.generic = p.generic_x | p.generic_y;
   cudaError_t e;
   for (int k = 0; k < 2; ++k) {
     if ((e = cudaMalloc(&p.tw_x[k], sizeof(float4) * std::max(nx, 32)))) return e;
@@ -1223,7 +1227,7 @@ HOLO_CHECK_TU(check_bits_kernels)
 cudaError_t fft_rows(const Plan& p, const float2* in, float2* out, long long nrows, bool inverse, float scale,
                      cudaStream_t s, const uint8_t* live, int rows_per_plane) {
   if (live && (rows_per_plane <= 0 || nrows >= (1LL << 31))) return cudaErrorInvalidValue;
-  if (p.generic) return g_fft_rows(p, in, out, nrows, inverse, scale, s, live, rows_per_plane);
+  if (p.generic_x) return g_fft_rows(p, in, out, nrows, inverse, scale, s, live, rows_per_plane);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.nx, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1278,7 +1282,7 @@ static size_t col_smem(int extra) {
 
 cudaError_t fft_cols(const Plan& p, const float2* in, float2* out, int nplanes, bool inverse, float scale,
                      cudaStream_t s) {
-  if (p.generic) return g_fft_cols(p, in, out, nplanes, inverse, scale, s);
+  if (p.generic_y) return g_fft_cols(p, in, out, nplanes, inverse, scale, s);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1320,7 +1324,7 @@ constexpr int kMaxRecur = 32;
 #define HOLO_FWD_C(N) ((N) <= HOLO_FWD_STAGED_MAX ? HOLO_FWD_CC : 4)
 
 cudaError_t adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed) {
-  if (p.generic) return g_adj_cols(p, R, out, nzl, k0, s, packed);
+  if (p.generic_y) return g_adj_cols(p, R, out, nzl, k0, s, packed);
   cudaError_t err = cudaSuccess;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {
     constexpr int N = decltype(nc)::value;
@@ -1377,7 +1381,7 @@ int fwd_groups(const Plan& p, int nzl) {
 
 cudaError_t fwd_cols(const Plan& p, const float2* in, float2* Spart, int nzl, int k0, int groups, cudaStream_t s,
                      bool packed, const uint8_t* live) {
-  if (p.generic) return g_fwd_cols(p, in, Spart, nzl, k0, groups, s, packed, live);
+  if (p.generic_y) return g_fwd_cols(p, in, Spart, nzl, k0, groups, s, packed, live);
   cudaError_t err = cudaSuccess;
   const int ppg = (nzl + groups - 1) / groups;
   const bool ok = dispatch_n(p.ny, [&](auto nc) {

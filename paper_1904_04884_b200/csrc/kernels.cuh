@@ -20,7 +20,9 @@ struct Plan {
   int any_propagating = 0;
   // general plane sizes (gfft.cu): a side that is not a power of two runs every
   // pass through the mixed-radix kernels; W_N roots per side
-  int generic = 0;
+  int generic = 0;    // either side runs gfft.cu
+  int generic_x = 0;  // rows (nx not a power of two)
+  int generic_y = 0;  // columns (ny not a power of two, or nx not a multiple of the fused passes' 8 columns)
   float2* groots_x = nullptr;
   float2* groots_y = nullptr;
 };

@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("nx,ny", [(96, 80), (100, 100), (210, 126), (1280, 24), (24, 1080), (122, 61), (1000, 8),
-                                   (99, 35), (1021, 8), (134, 67)])
+                                   (99, 35), (1021, 8), (134, 67),
+                                   (96, 64), (64, 96), (100, 64)])  # one fused side (see Plan::generic_x / _y)
 def test_fft2_general_sizes(nx, ny):
     from paper_1904_04884_b200 import VolumeGeometry
     from paper_1904_04884_b200.engine import HoloEngine
@@ -35,7 +36,8 @@ def _largest_prime(n):
     return best
 
 
-@pytest.mark.parametrize("nx,ny,nz", [(100, 60, 5), (96, 200, 3), (1280, 40, 2)])
+@pytest.mark.parametrize("nx,ny,nz", [(100, 60, 5), (96, 200, 3), (1280, 40, 2),
+                                      (1280, 64, 2), (64, 1080, 2)])  # mixed-radix rows + fused TMA columns, and back
 def test_forward_adjoint_general_sizes_vs_oracle(nx, ny, nz):
     from paper_1904_04884_b200 import VolumeGeometry
     from paper_1904_04884_b200.engine import HoloEngine
@@ -57,6 +59,8 @@ def test_forward_adjoint_general_sizes_vs_oracle(nx, ny, nz):
                                               ((99, 70, 3), 5, False),     # odd nx: generic tile prox
                                               ((75, 66, 3), 13, True),     # odd nx, real engine, T = 13
                                               ((134, 67, 2), 5, False),    # prime factors 67 (direct DFT lines)
+                                              ((96, 64, 3), 5, False),     # mixed-radix rows, fused columns
+                                              ((64, 96, 4), 13, True),     # fused rows, mixed-radix columns, real
                                               ((1000, 1000, 2), 5, False)])  # a 1000x1000 camera frame
 def test_fista_general_sizes_vs_oracle(shape, inner, real):
     from paper_1904_04884_b200 import ComplexField2D, RegularizerWeights, SolverConfig, VolumeGeometry, fista
