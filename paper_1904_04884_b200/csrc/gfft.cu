@@ -262,6 +262,49 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
   }
 }
 
+// adjoint: out[k] = colIFFT(U_k R) for the CTA's planes [kb, ke); R and the
+// phase are plane-independent and stay in registers across the planes
+__global__ void __launch_bounds__(kGThreads, 2) k_gadj(const float2* __restrict__ R, float2* out, int nx, int N, int L,
+                                                       Radices rad, const float2* __restrict__ Wg, int nzl, int ppc,
+                                                       const uint64_t* __restrict__ tab,
+                                                       const float2* __restrict__ circ, int k0, bool packed) {
+  extern __shared__ __align__(16) float2 gsm[];
+  float2* W = gsm;
+  float2* a = gsm + N;
+  float2* b = a + (size_t)L * N;
+  load_roots(W, Wg, N);
+  const int lgL = __ffs(L) - 1;  // L is a power of two
+  const int c0 = blockIdx.x * L, kb = blockIdx.y * ppc, ke = min(nzl, kb + ppc);
+  const long long P = (long long)nx * N;
+  constexpr int kReg = (kGLineElems > kGMaxN ? kGLineElems : kGMaxN) / kGThreads;
+  float2 rv[kReg];
+  uint64_t ph[kReg];
+#pragma unroll
+  for (int n = 0; n < kReg; ++n) {
+    const int t = threadIdx.x + n * kGThreads;
+    const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
+    const bool on = t < L * N && c < nx;
+    rv[n] = on ? R[(long long)i * nx + c] : czero();
+    ph[n] = on ? tab[(long long)i * nx + c] : 0ull;
+  }
+  for (int k = kb; k < ke; ++k) {
+    __syncthreads();  // the previous plane's result buffer has been stored
+#pragma unroll
+    for (int n = 0; n < kReg; ++n) {
+      const int t = threadIdx.x + n * kGThreads;
+      const int l = t & (L - 1), i = t >> lgL;
+      if (t < L * N) a[l * N + i] = cmul(rv[n], plane_weight(ph[n], k0, k, packed, circ));
+    }
+    __syncthreads();
+    const float2* res = stockham(a, b, N, L, rad, W, true);
+    float2* dst = out + (long long)k * P;
+    for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+      const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
+      if (c < nx) dst[(long long)i * nx + c] = res[l * N + i];
+    }
+  }
+}
+
 // forward: Spart[g] = sum_{k in group g, live} colFFT(in[k]) conj(U_k)
 __global__ void __launch_bounds__(kGThreads, 3) k_gfwd(const float2* in, float2* Spart, int nx, int N, int L, Radices rad,
                                                     const float2* __restrict__ Wg, int nzl, int ppg,
@@ -370,12 +413,16 @@ cudaError_t g_fft_cols(const Plan& p, const float2* in, float2* out, int nplanes
 cudaError_t g_adj_cols(const Plan& p, const float2* R, float2* out, int nzl, int k0, cudaStream_t s, bool packed) {
   const int N = p.ny, L = lines_per_cta(N);
   const size_t smem = smem_bytes(N, L, 2);
-  cudaError_t e = allow_smem(k_gcols, smem);
+  cudaError_t e = allow_smem(k_gadj, smem);
   if (e) return e;
   if (nzl <= 0) return cudaSuccess;
-  dim3 grid((p.nx + L - 1) / L, nzl);
-  k_gcols<<<grid, kGThreads, smem, s>>>(R, out, p.nx, N, L, factor(N), p.groots_y, true, 1.0f, 1, p.phase, p.circle,
-                                        k0, packed);
+  const int bx = (p.nx + L - 1) / L;
+  // plane groups: ~8 waves of 2 CTAs per SM, R and the phase reused across a group
+  const int groups = std::max(1, std::min(nzl, (148 * 2 * 8 + bx - 1) / bx));
+  const int ppc = (nzl + groups - 1) / groups;
+  dim3 grid(bx, (nzl + ppc - 1) / ppc);
+  k_gadj<<<grid, kGThreads, smem, s>>>(R, out, p.nx, N, L, factor(N), p.groots_y, nzl, ppc, p.phase, p.circle, k0,
+                                       packed);
   add_launches(1);
   return cudaGetLastError();
 }
