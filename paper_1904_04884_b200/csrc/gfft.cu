@@ -228,12 +228,10 @@ __global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* o
   }
 }
 
-// columns: CTA = L adjacent columns of one plane (blockIdx.y), N = ny points.
-// mode 0: out[k] = scale * colFFT(in[k]); mode 1 (adjoint): out[k] = colIFFT(U_k R)
+// columns: CTA = L adjacent columns of one plane (blockIdx.y), N = ny points:
+// out[k] = scale * colFFT(in[k])
 __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* out, int nx, int N, int L, Radices rad,
-                                                     const float2* __restrict__ Wg, bool inv, float scale, int mode,
-                                                     const uint64_t* __restrict__ tab,
-                                                     const float2* __restrict__ circ, int k0, bool packed) {
+                                                     const float2* __restrict__ Wg, bool inv, float scale) {
   extern __shared__ __align__(16) float2 gsm[];
   float2* W = gsm;
   float2* a = gsm + N;
@@ -242,16 +240,10 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
   const int lgL = __ffs(L) - 1;  // L is a power of two
   const int c0 = blockIdx.x * L, k = blockIdx.y;
   const long long P = (long long)nx * N;
-  const float2* src = mode == 1 ? in : in + (long long)k * P;
+  const float2* src = in + (long long)k * P;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
     const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
-    float2 v = czero();
-    if (c < nx) {
-      const long long p = (long long)i * nx + c;
-      v = src[p];
-      if (mode == 1) v = cmul(v, plane_weight(tab[p], k0, k, packed, circ));
-    }
-    a[l * N + i] = v;
+    a[l * N + i] = c < nx ? src[(long long)i * nx + c] : czero();
   }
   __syncthreads();
   const float2* res = stockham(a, b, N, L, rad, W, inv);
@@ -404,8 +396,7 @@ cudaError_t g_fft_cols(const Plan& p, const float2* in, float2* out, int nplanes
   if (e) return e;
   if (nplanes <= 0) return cudaSuccess;
   dim3 grid((p.nx + L - 1) / L, nplanes);
-  k_gcols<<<grid, kGThreads, smem, s>>>(in, out, p.nx, N, L, factor(N), p.groots_y, inverse, scale, 0, p.phase,
-                                        p.circle, 0, false);
+  k_gcols<<<grid, kGThreads, smem, s>>>(in, out, p.nx, N, L, factor(N), p.groots_y, inverse, scale);
   add_launches(1);
   return cudaGetLastError();
 }
