@@ -39,6 +39,9 @@ CONFIGS = {
     "c3": (1024, 1024, 512, 100, 0.2, 2, 0.5, 0.2, 5, 20e-6),
     "c4": (2048, 2048, 1000, 100, 0.05, 3, 0.5, 0.2, 5, 20e-6),  # 134 GB of state on one B200 (8 GPUs in BASELINE)
     "c5": (1024, 1024, 512, 100, 0.05, 4, 0.05, 1.0, 20, 20e-6),  # rods (microfibers), length 10 d
+    # a 1280x1024 camera frame (not a BASELINE config): C3's volume depth and weights,
+    # mixed-radix rows (csrc/gfft.cu) with the fused column passes
+    "cam": (1280, 1024, 512, 100, 0.2, 5, 0.5, 0.2, 5, 20e-6),
 }
 METRIC = "voxel-iterations/sec (1024²×512 fused-lasso FISTA) at 1/2/4/8 B200; % HBM roofline"
 BYTES_PER_VOXEL_ITER = 72  # SURVEY.md 8(d) algorithmic bytes per voxel-iteration
@@ -50,8 +53,9 @@ def n_particles(cfg):
     nx, _, _, _, sd, _, _, _, inner, d = cfg
     if sd is None:
         return 50
+    ny = cfg[1]
     area = d ** 2 if cfg is not CONFIGS.get("c5") else 7.9 * d ** 2  # mean projected rod area ~ pi/4 * 10 d^2
-    return int(round(sd * (nx * PITCH) ** 2 / area))
+    return int(round(sd * nx * ny * PITCH ** 2 / area))
 
 
 def make_hologram(cfg, device=None):
