@@ -10,9 +10,9 @@
 //    (R, Ns) maps butterfly j to outputs (j / Ns) Ns R + j % Ns + q Ns with the
 //    combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)) from one fp64-exact
 //    table of the N roots of unity: a stage twiddle per input, then an
-//    in-register radix-2/3/4 (closed form) or radix-5/7 (table) DFT; larger
-//    prime factors re-read their inputs, R^2 table MACs (a prime side is a
-//    direct DFT of its lines);
+//    in-register radix-2/3/4 (closed form) or radix-5/7 (table) DFT; a larger
+//    prime factor R gives each thread one output of R table MACs over
+//    re-read inputs (a prime side is a direct DFT of its lines);
 //  * the adjoint multiplies R by the plane weight U_k on the load (complex
 //    engine: H_{k0+k}; packed real engine: Re H_j + i Re H_{j+1}, j = k0 + 2k),
 //    the forward accumulates colFFT(v_k) conj(U_k) over a CTA's plane group in
@@ -44,7 +44,7 @@ struct Radices {
   int n = 0;
   int r[24] = {};
   int M[24] = {}, Ns[24] = {}, step[24] = {};
-  unsigned mM[24] = {}, mNs[24] = {};
+  unsigned mM[24] = {}, mNs[24] = {}, mR[24] = {};
 };
 
 unsigned magic(int d) { return d >= 2 ? (unsigned)((0x100000000ull + (unsigned long long)d - 1) / (unsigned long long)d) : 0u; }
@@ -62,6 +62,7 @@ Radices factor(int N) {
     f.step[s] = N / (ns * f.r[s]);
     f.mM[s] = magic(f.M[s]);
     f.mNs[s] = magic(ns);
+    f.mR[s] = magic(f.r[s]);
     ns *= f.r[s];
   }
   return f;
@@ -143,22 +144,21 @@ __device__ __forceinline__ void bfly(const float2* sl, float2* dl, int j, int M,
   for (int q = 0; q < R; ++q) dl[base + q * Ns] = x[q];
 }
 
-// large prime radix: inputs re-read from shared memory, R^2 table MACs
-__device__ void bfly_any(const float2* sl, float2* dl, int j, int M, int jm, int Ns, int step, int base, int R,
+// large prime radix: one output q of butterfly j per call (so a prime side's
+// R outputs spread over R threads), R table MACs re-reading the inputs
+__device__ void bfly_one(const float2* sl, float2* dl, int j, int q, int M, int jm, int Ns, int step, int base, int R,
                          const float2* W, bool inv, int N) {
-  for (int q = 0; q < R; ++q) {
-    const int e = (jm + q * Ns) * step;  // < N
-    float2 acc = czero();
-    int m = 0;
-    for (int r = 0; r < R; ++r) {
-      const float2 x = sl[j + r * M];
-      const float2 w = conj_if(W[m], inv);
-      acc = make_float2(fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x)), fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y)));
-      m += e;
-      if (m >= N) m -= N;
-    }
-    dl[base + q * Ns] = acc;
+  const int e = (jm + q * Ns) * step;  // < N
+  float2 acc = czero();
+  int m = 0;
+  for (int r = 0; r < R; ++r) {
+    const float2 x = sl[j + r * M];
+    const float2 w = conj_if(W[m], inv);
+    acc = make_float2(fmaf(x.x, w.x, fmaf(-x.y, w.y, acc.x)), fmaf(x.x, w.y, fmaf(x.y, w.x, acc.y)));
+    m += e;
+    if (m >= N) m -= N;
   }
+  dl[base + q * Ns] = acc;
 }
 
 // L lines of N points in a (line-major [L][N]); returns the buffer holding the result
@@ -168,18 +168,27 @@ __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& r
   for (int s = 0; s < rad.n; ++s) {
     const int R = rad.r[s], M = rad.M[s], Ns = rad.Ns[s], step = rad.step[s];
     const unsigned mM = rad.mM[s], mNs = rad.mNs[s];
-    for (int t = threadIdx.x; t < L * M; t += blockDim.x) {
-      const int line = udiv(t, M, mM), j = t - line * M;
-      const float2* sl = src + line * N;
-      float2* dl = dst + line * N;
-      const int jq = udiv(j, Ns, mNs), jm = j - jq * Ns, base = jq * Ns * R + jm;
-      switch (R) {
-        case 2: bfly<2>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-        case 3: bfly<3>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-        case 4: bfly<4>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-        case 5: bfly<5>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-        case 7: bfly<7>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-        default: bfly_any(sl, dl, j, M, jm, Ns, step, base, R, W, inv, N);
+    if (R <= 7) {
+      for (int t = threadIdx.x; t < L * M; t += blockDim.x) {
+        const int line = udiv(t, M, mM), j = t - line * M;
+        const float2* sl = src + line * N;
+        float2* dl = dst + line * N;
+        const int jq = udiv(j, Ns, mNs), jm = j - jq * Ns, base = jq * Ns * R + jm;
+        switch (R) {
+          case 2: bfly<2>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+          case 3: bfly<3>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+          case 4: bfly<4>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+          case 5: bfly<5>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+          default: bfly<7>(sl, dl, j, M, jm, Ns, step, base, W, inv, N);
+        }
+      }
+    } else {  // prime R > 7: tasks are (line, butterfly, output), L N of them
+      const unsigned mR = rad.mR[s];
+      for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
+        const int lj = udiv(t, R, mR), q = t - lj * R;
+        const int line = udiv(lj, M, mM), j = lj - line * M;
+        const int jq = udiv(j, Ns, mNs), jm = j - jq * Ns, base = jq * Ns * R + jm;
+        bfly_one(src + line * N, dst + line * N, j, q, M, jm, Ns, step, base, R, W, inv, N);
       }
     }
     __syncthreads();
