@@ -1003,7 +1003,7 @@ int holo_version(void) { return 1; }
 
 int holo_debug_checks(uint32_t* bits) {
   cudaDeviceSynchronize();
-  const unsigned v = holo::check_bits_kernels() | holo::check_bits_prox();
+  const unsigned v = holo::check_bits_kernels() | holo::check_bits_prox() | holo::check_bits_gfft();
   if (bits) *bits = v;
 #ifdef HOLO_CHECKS
   return 1;

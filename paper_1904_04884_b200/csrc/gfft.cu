@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* o
                                                      float scale, const uint8_t* __restrict__ live,
                                                      int rows_per_plane) {
   extern __shared__ __align__(16) float2 gsm[];
+  poison_dyn_smem();
   float2* W = gsm;
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* o
   for (int l = 0; l < L; ++l) {
     const long long row = r0 + l;
     const bool on = row < nrows && !(live && !live[row / rows_per_plane]);
+    HOLO_DCHECK(!on || (row + 1) * N <= nrows * N, CK_ROWS);
     for (int i = threadIdx.x; i < N; i += blockDim.x) a[l * N + i] = on ? in[row * N + i] : czero();
   }
   __syncthreads();
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kGThreads) k_grows(const float2* in, float2* o
 __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* out, int nx, int N, int L, Radices rad,
                                                      const float2* __restrict__ Wg, bool inv, float scale) {
   extern __shared__ __align__(16) float2 gsm[];
+  poison_dyn_smem();
   float2* W = gsm;
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(kGThreads) k_gcols(const float2* in, float2* o
   float2* dst = out + (long long)k * P;
   for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
     const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
+    HOLO_DCHECK(i < N, CK_COLS);
     if (c < nx) dst[(long long)i * nx + c] = cscale(res[l * N + i], scale);
   }
 }
@@ -270,6 +274,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_gadj(const float2* __restrict_
                                                        const uint64_t* __restrict__ tab,
                                                        const float2* __restrict__ circ, int k0, bool packed) {
   extern __shared__ __align__(16) float2 gsm[];
+  poison_dyn_smem();
   float2* W = gsm;
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(kGThreads, 2) k_gadj(const float2* __restrict_
     float2* dst = out + (long long)k * P;
     for (int t = threadIdx.x; t < L * N; t += blockDim.x) {
       const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
+      HOLO_DCHECK(i < N && k < nzl, CK_COLS);
       if (c < nx) dst[(long long)i * nx + c] = res[l * N + i];
     }
   }
@@ -313,6 +319,7 @@ __global__ void __launch_bounds__(kGThreads, 3) k_gfwd(const float2* in, float2*
                                                     const float2* __restrict__ circ, int k0, bool packed,
                                                     const uint8_t* __restrict__ live) {
   extern __shared__ __align__(16) float2 gsm[];
+  poison_dyn_smem();
   float2* W = gsm;
   float2* a = gsm + N;
   float2* b = a + (size_t)L * N;
@@ -350,6 +357,7 @@ __global__ void __launch_bounds__(kGThreads, 3) k_gfwd(const float2* in, float2*
   for (int n = 0; n < kAcc; ++n) {
     const int t = threadIdx.x + n * kGThreads;
     const int l = t & (L - 1), i = t >> lgL, c = c0 + l;
+    HOLO_DCHECK(t >= L * N || i < N, CK_COLS);
     if (t < L * N && c < nx) dst[(long long)i * nx + c] = acc[n];
   }
 }
@@ -368,6 +376,8 @@ cudaError_t allow_smem(K kern, size_t bytes) {
 }
 
 }  // namespace
+
+HOLO_CHECK_TU(check_bits_gfft)
 
 bool pow2_side(int n) { return n >= 8 && n <= 4096 && (n & (n - 1)) == 0; }
 

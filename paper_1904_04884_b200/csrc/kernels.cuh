@@ -127,6 +127,7 @@ void plan_free(Plan& p);
 // translation unit (HoloCheckBit, common.cuh); 0 in the normal build
 unsigned check_bits_kernels();
 unsigned check_bits_prox();
+unsigned check_bits_gfft();
 
 // batched 1D transforms (unnormalised; `scale` multiplies the output)
 // live (optional, forward rows): live[row / rows_per_plane] == 0 marks an

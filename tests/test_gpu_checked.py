@@ -4,7 +4,7 @@ compute-sanitizer substitute: compute-sanitizer is closed on the GPU pool.
 tools/checked_solve.py runs small solves over every kernel family -- the
 single-pass and multi-pass strip prox, the generic prox, the packed real
 engine, plane skipping, the in-process rank group's peer-memory plane sum and
-the guard fix-up -- once with the normal library and once with the checked one,
+the guard fix-up, the mixed-radix passes of general plane sides -- once with the normal library and once with the checked one,
 in which every kernel tests its global indices and tensor-copy frames against
 the buffers' bounds, the prox / FFT kernels fill their shared memory with NaN
 before use and the engine fills fresh device buffers with 0xFF (NaN).  The two
@@ -41,4 +41,4 @@ def test_checked_build_matches_and_reports_no_violations():
     assert normal[-1] == "checked-build 0 check-bits 0x0", normal[-1]
     assert checked[-1] == "checked-build 1 check-bits 0x0", checked[-1]
     assert normal[:-1] == checked[:-1]
-    assert len(normal) == 8
+    assert len(normal) == 10

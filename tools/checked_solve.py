@@ -11,6 +11,7 @@ of the solution bytes) and the check bits last.  Cases:
   skip     128x128x16, T = 5   all-zero planes skipped by the forward passes
   group    128x128x6,  2 ranks in-process rank group (peer-memory scatter / gather)
   guard    256x256x1   guard fix-up (forced prox rerun) on the strip kernel
+  gsides   100x72x4 and 99x70x3 (packed real)  mixed-radix passes (gfft.cu), odd nx
 """
 import ctypes
 import hashlib
@@ -76,7 +77,7 @@ def group(nx, ny, nz, nranks):
 
 if __name__ == "__main__":
     torch.cuda.init()
-    which = sys.argv[1:] or ["strip", "walk", "generic", "real", "skip", "group", "guard"]
+    which = sys.argv[1:] or ["strip", "walk", "generic", "real", "skip", "group", "guard", "gsides"]
     if "strip" in which:
         solve("strip", 128, 128, 8, 5)
     if "walk" in which:
@@ -94,6 +95,9 @@ if __name__ == "__main__":
         b[60:140, 90:200] = 1.0
         rep = solve("guard", 256, 256, 1, 5, lam=(0.02, 1.0), iters=2, z0=0.0, b=b)
         assert rep.guard_fixups > 0
+    if "gsides" in which:
+        solve("gsides", 100, 72, 4, 5)
+        solve("gsides-real", 99, 70, 3, 5, lam=(0.3, 0.2), real=True, step=1.0 / 12)
     v = ctypes.c_uint32(0)
     checked = nat.load().holo_debug_checks(ctypes.byref(v))
     print(f"checked-build {checked} check-bits {v.value:#x}", flush=True)
