@@ -6,11 +6,11 @@
 // semantics as fft_rows / fft_cols / adj_cols / fwd_cols (kernels.cuh):
 //
 //  * each line (row or column) is transformed in shared memory by a Stockham
-//    autosort over the prime factors of N (radix 4 for pairs of 2s): stage
+//    autosort over the factors of N (radix 8, then 4, for the 2s): stage
 //    (R, Ns) maps butterfly j to outputs (j / Ns) Ns R + j % Ns + q Ns with the
 //    combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)) from one fp64-exact
 //    table of the N roots of unity: a stage twiddle per input, then an
-//    in-register radix-2/3/4 (closed form) or radix-5/7 (table) DFT; a larger
+//    in-register radix-2/3/4/8 (closed form) or radix-5/7 (table) DFT; a larger
 //    prime factor R gives each thread one output of R table MACs over
 //    re-read inputs (a prime side is a direct DFT of its lines);
 //  * the adjoint multiplies R by the plane weight U_k on the load (complex
@@ -52,6 +52,7 @@ unsigned magic(int d) { return d >= 2 ? (unsigned)((0x100000000ull + (unsigned l
 Radices factor(int N) {
   Radices f;
   int n = N;
+  while (n % 8 == 0 && n > 8) { f.r[f.n++] = 8; n /= 8; }
   while (n % 4 == 0 && n > 4) { f.r[f.n++] = 4; n /= 4; }
   for (int p = 2; n > 1; ++p)
     while (n % p == 0) { f.r[f.n++] = p; n /= p; }
@@ -116,6 +117,30 @@ __device__ __forceinline__ void bfly(const float2* sl, float2* dl, int j, int M,
     x[2] = csub(a, c);
     x[1] = cadd(b, di);
     x[3] = csub(b, di);
+  } else if constexpr (R == 8) {  // two 4-point DFTs (even / odd inputs) and W_8^q
+    float2 ev[4] = {x[0], x[2], x[4], x[6]}, od[4] = {x[1], x[3], x[5], x[7]};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float2* v = h ? od : ev;
+      const float2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]), c = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+      const float2 di = inv ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+      v[0] = cadd(a, c);
+      v[2] = csub(a, c);
+      v[1] = cadd(b, di);
+      v[3] = csub(b, di);
+    }
+    const float h = 0.70710678118654752f, sg = inv ? 1.f : -1.f;
+    const float2 o1 = make_float2(h * (od[1].x - sg * od[1].y), h * (od[1].y + sg * od[1].x));   // W_8 o1
+    const float2 o2 = make_float2(-sg * od[2].y, sg * od[2].x);                                  // W_8^2 o2
+    const float2 o3 = make_float2(h * (-od[3].x - sg * od[3].y), h * (-od[3].y + sg * od[3].x));  // W_8^3 o3
+    x[0] = cadd(ev[0], od[0]);
+    x[4] = csub(ev[0], od[0]);
+    x[1] = cadd(ev[1], o1);
+    x[5] = csub(ev[1], o1);
+    x[2] = cadd(ev[2], o2);
+    x[6] = csub(ev[2], o2);
+    x[3] = cadd(ev[3], o3);
+    x[7] = csub(ev[3], o3);
   } else if constexpr (R == 3) {
     const float sn = inv ? 0.86602540378443865f : -0.86602540378443865f;  // Im W_3
     const float2 t = cadd(x[1], x[2]), u = csub(x[1], x[2]);
@@ -168,7 +193,7 @@ __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& r
   for (int s = 0; s < rad.n; ++s) {
     const int R = rad.r[s], M = rad.M[s], Ns = rad.Ns[s], step = rad.step[s];
     const unsigned mM = rad.mM[s], mNs = rad.mNs[s];
-    if (R <= 7) {
+    if (R <= 8) {
       for (int t = threadIdx.x; t < L * M; t += blockDim.x) {
         const int line = udiv(t, M, mM), j = t - line * M;
         const float2* sl = src + line * N;
@@ -179,7 +204,8 @@ __device__ float2* stockham(float2* a, float2* b, int N, int L, const Radices& r
           case 3: bfly<3>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
           case 4: bfly<4>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
           case 5: bfly<5>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
-          default: bfly<7>(sl, dl, j, M, jm, Ns, step, base, W, inv, N);
+          case 7: bfly<7>(sl, dl, j, M, jm, Ns, step, base, W, inv, N); break;
+          default: bfly<8>(sl, dl, j, M, jm, Ns, step, base, W, inv, N);
         }
       }
     } else {  // prime R > 7: tasks are (line, butterfly, output), L N of them

@@ -1,8 +1,8 @@
 """CPU model of the mixed-radix Stockham passes in csrc/gfft.cu (general plane
-sides): the same factorisation (4s first, then primes), stage index map
+sides): the same factorisation (8s, then 4s, then primes), stage index map
 (butterfly j reads j + r N/R, writes (j // Ns) Ns R + j % Ns + q Ns) and
 combined twiddle W_N^(r (j % Ns + q Ns) N / (Ns R)), checked against numpy's
-FFT for the radices the kernels meet (2, 3, 4, 5, 7, larger primes).  The CUDA
+FFT for the radices the kernels meet (2, 3, 4, 5, 7, 8, larger primes).  The CUDA
 kernels themselves are checked on the GPU by tests/test_gpu_general_sizes.py."""
 import numpy as np
 import pytest
@@ -10,6 +10,9 @@ import pytest
 
 def factor(n):
     f = []
+    while n % 8 == 0 and n > 8:
+        f.append(8)
+        n //= 8
     while n % 4 == 0 and n > 4:
         f.append(4)
         n //= 4
@@ -40,7 +43,7 @@ def stockham(x, inverse=False):
     return src
 
 
-@pytest.mark.parametrize("n", [8, 12, 30, 64, 96, 100, 125, 210, 1000, 1021, 1080, 1280, 134, 61 * 2])
+@pytest.mark.parametrize("n", [8, 12, 30, 64, 96, 100, 125, 210, 1000, 1021, 1080, 1280, 1536, 134, 61 * 2])
 def test_stockham_model_matches_numpy(n):
     rng = np.random.default_rng(n)
     x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
@@ -52,4 +55,4 @@ def test_factorisation_products():
     for n in range(8, 4097, 37):
         f = factor(n)
         assert int(np.prod(f)) == n
-        assert all(r == 4 for r in f[:f.count(4)])
+        assert f == sorted(f, key=lambda r: (r not in (8, 4), r != 8))  # 8s, 4s, then the rest
